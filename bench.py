@@ -1,0 +1,436 @@
+"""Benchmark: batched pROST per-frame update on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+One step = one frame for every stream of the workload (the BASELINE config
+named by --config; default C3: 256 independent 320x240 grayscale streams,
+k=15, p=0.5, mu=1e-4, 2 CG iterations).  Streams shard across ranks with no
+collective (weak scaling: every rank runs its own `--streams` streams).  Rank 0
+prints one JSON line.
+
+`value`: stream-frames/s over all ranks, frames already resident in HBM,
+device-timed with CUDA events (max over ranks).  `e2e`: the same through the
+public API with pinned HOST frames in and host mask + background out, copies
+inside the timed region.  `roofline`: algorithmic bytes of the frame update
+(B_alg = 8nk + 12n + 3P per stream-frame) over the measured
+step time against MEASURED_PEAKS.json's HBM copy bandwidth.  `cpu_baseline`:
+the numpy oracle port of the reference path on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PHASE_BYTES_NOTE = "per-phase algorithmic bytes per stream-frame launch"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--streams", type=int, default=None, help="streams per rank")
+    ap.add_argument("--frames", type=int, default=8, help="distinct frames staged per stream")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--cpu-frames", type=int, default=12, help="oracle frames per CPU worker")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--wave", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def workload(name, streams):
+    from paper_1302_2073_b200.synth import CONFIGS
+
+    c = CONFIGS[name]
+    S = streams if streams is not None else c["streams"]
+    t = dict(c["tracker"])
+    return c, S, t
+
+
+def gen_frames(name, stream_ids, n_frames, dtype=np.float32):
+    from paper_1302_2073_b200.synth import SceneStream, config_spec
+
+    out = None
+    for i, sid in enumerate(stream_ids):
+        f = SceneStream(config_spec(name, sid), dtype=dtype).next_frames(n_frames)
+        if out is None:
+            out = np.empty((n_frames, len(stream_ids), f.shape[1]), dtype=dtype)
+        out[:, i] = f
+    return out
+
+
+def b_alg(n, k, P):
+    """U read+write + x + mean + background + 3 label bytes."""
+    return 8 * n * k + 12 * n + 3 * P
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port, one stream per worker process
+
+
+def _cpu_worker(job):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    name, sid, n_frames, tracker = job
+    sys.path.insert(0, str(ROOT))
+    from oracle import prost_oracle as orc
+    from paper_1302_2073_b200.params import RunConfig
+
+    frames = gen_frames(name, [sid], n_frames + 1, dtype=np.float64)[:, 0]
+    cfg = RunConfig(**tracker)
+    prm = cfg.params(100)
+    W, H = cfg.target_width, cfg.target_height
+    ch = 1 if cfg.grayscale else 3
+    ref = orc.PipelineOracle(W, H, ch, orc.OracleParams(
+        k=prm.k, p=prm.cfg.p, mu=prm.cfg.mu, delta=prm.delta, omega=prm.omega,
+        t_init=prm.t_init, t_min=prm.t_min, tau=prm.tau, max_iters=prm.cg.max_iters),
+        i_init=100, seed=cfg.seed)
+    ref.push(frames[0])  # bootstrap (basis QR) outside the timed part
+    t0 = time.perf_counter()
+    for f in frames[1:]:
+        ref.push(f)
+        ref.background()
+    return n_frames, time.perf_counter() - t0
+
+
+def cpu_rate(name, tracker, n_frames, cores=None):
+    import multiprocessing as mp
+
+    cores = cores or len(os.sched_getaffinity(0))
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    jobs = [(name, sid, n_frames, tracker) for sid in range(cores)]
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    frames = sum(r[0] for r in res)
+    slowest = max(r[1] for r in res)
+    return frames / slowest, cores, frames, wall
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    c, S, tracker = workload(args.config, args.streams)
+    if rank != 0:
+        return 0
+    cores = len(os.sched_getaffinity(0))
+    # each step: one frame for `cores` streams (one worker process each)
+    n_frames = args.warmup + args.steps
+    rate, cores, frames, wall = cpu_rate(args.config, tracker, n_frames, cores)
+    W, H = tracker["target_width"], tracker["target_height"]
+    P = W * H
+    line = {
+        "impl": "reference", "metric": "frames/s", "value": rate, "unit": "stream-frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * cores / rate, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d) model)",
+        "config": {"workload": f"{args.config}: {W}x{H} gray, k={tracker['subspace_dim']}, "
+                               f"p={tracker['p']}, mu={tracker['mu']}, cg={tracker['cg_max_iters']}",
+                   "streams_per_step": cores},
+        "mpix_per_s": rate * P / 1e6,
+        "cpu_baseline": {"value": rate, "unit": "stream-frames/s", "cores": cores,
+                         "kind": "port", "cpu": cpu_model(),
+                         "sample": f"{cores} worker processes x {n_frames} frames of their own "
+                                   f"{args.config} stream (numpy oracle, OPENBLAS_NUM_THREADS=1)"},
+        "e2e": {"value": rate, "unit": "stream-frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    import paper_1302_2073_b200 as pkg
+
+    c, S, tracker = workload(args.config, args.streams)
+    cfg = pkg.RunConfig(i_init=100, **tracker)
+    W, H = cfg.target_width, cfg.target_height
+    ch = 1 if cfg.grayscale else 3
+    P = W * H
+    n = P * ch
+    k = cfg.subspace_dim
+    stream_ids = list(range(rank * S, (rank + 1) * S))
+
+    t_gen = time.perf_counter()
+    host = gen_frames(args.config, stream_ids, args.frames)  # [F, S, n] float32
+    t_gen = time.perf_counter() - t_gen
+    frames_dev = torch.from_numpy(host).to(f"cuda:{dev}")
+    bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev)
+    if args.wave:
+        bt.native.set_wave(args.wave)
+    mask = torch.empty((S, P), dtype=torch.uint8, device=f"cuda:{dev}")
+    bg = torch.empty((S, n), dtype=torch.float32 if args.precision == "fp32" else torch.float64,
+                     device=f"cuda:{dev}")
+    if args.precision == "fp64":
+        frames_dev = frames_dev.double()
+    F = args.frames
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if ws == 1:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step = 0
+    for _ in range(args.warmup):
+        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        step += 1
+    torch.cuda.synchronize()
+    bt.synchronize()
+
+    clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)).split(",")[0])
+                    if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else dev)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = bt.native.launches
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        step += 1
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = bt.native.launches - launches0
+    clk = clocks.stop()
+    ms = max_over_ranks(ms)
+    ms_step = ms / args.steps
+    value = ws * S * args.steps / (ms / 1000.0)
+
+    # per-phase breakdown (separate, untimed pass with events around launches)
+    bt.native.profile(True)
+    for _ in range(3):
+        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        step += 1
+    torch.cuda.synchronize()
+    phases = bt.native.profile_read()
+    bt.native.profile(False)
+
+    # end to end through the public API: pinned host frames in, host mask + bg out
+    e2e = None
+    if not args.no_e2e:
+        host_pinned = torch.from_numpy(host).pin_memory()
+        if args.precision == "fp64":
+            host_pinned = host_pinned.double().pin_memory()
+        mask_h = torch.empty((S, P), dtype=torch.uint8).pin_memory()
+        bg_h = torch.empty((S, n), dtype=bg.dtype).pin_memory()
+        for _ in range(2):
+            bt.push(host_pinned[step % F], background=bg_h, mask=mask_h)
+            step += 1
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            bt.push(host_pinned[step % F], background=bg_h, mask=mask_h)
+            step += 1
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": ws * S * args.steps / (ms_e2e / 1000.0), "unit": "stream-frames/s",
+               "h2d_bytes_per_step": S * n * host_pinned.element_size(),
+               "d2h_bytes_per_step": S * P + S * n * bg_h.element_size(),
+               "ms_per_step": ms_e2e / args.steps}
+    bt.synchronize()
+
+    # roofline of the frame update (per GPU)
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    if peaks_path.exists():
+        peak = float(json.loads(peaks_path.read_text())["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    else:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    ba = b_alg(n, k, P)
+    achieved = S * ba / (ms_step / 1000.0) / 1e9
+    bu = 8 * n * k
+    traffic = None
+    tpath = ROOT / "profiles" / "traffic.json"
+    if tpath.exists():
+        try:
+            tj = json.loads(tpath.read_text())
+            if tj.get("config") == args.config and tj.get("streams") == S:
+                traffic = tj.get("bytes_per_step")
+        except Exception:
+            traffic = None
+    tot_ms = sum(v[0] for v in phases.values()) or 1.0
+    phase_out = {nm: {"ms_per_step": v[0] / 3, "launches_per_step": v[1] / 3,
+                      "share": v[0] / tot_ms} for nm, v in phases.items() if v[1]}
+    dom = max(phase_out, key=lambda nm: phase_out[nm]["ms_per_step"]) if phase_out else None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            rate, cores, frames, wall = cpu_rate(args.config, tracker, args.cpu_frames)
+            cpu = {"value": rate, "unit": "stream-frames/s", "cores": cores, "kind": "port",
+                   "cpu": cpu_model(),
+                   "sample": f"{cores} worker processes x {args.cpu_frames} frames of their own "
+                             f"{args.config} stream (numpy oracle of the reference path, "
+                             f"OPENBLAS_NUM_THREADS=1; {wall:.1f} s wall)"}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "stream-frames/s", "cores": None, "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": "frames/s", "value": value, "unit": "stream-frames/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "fp32" else "f64",
+            "data": f"synthetic (seeded SURVEY.md §8(d) generator, {F} distinct frames per stream "
+                    "staged in HBM and cycled)",
+            "config": {"workload": f"{args.config}: {S} streams/GPU x {W}x{H}x{ch}, k={k}, "
+                                   f"p={cfg.p}, mu={cfg.mu}, cg_max_iters={cfg.cg_max_iters}",
+                       "streams_per_gpu": S, "n": n, "k": k, "precision": args.precision,
+                       "l2": "inputs larger than L2 (U alone is %.2f GB per GPU)" % (S * 4 * n * k / 1e9),
+                       "parallelism": f"stream-sharded x{ws}"},
+            "mpix_per_s": value * P / 1e6,
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "frame update (all phase kernels of one step)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_stream_frame": ba, "b_u_frac": (S * bu / (ms_step / 1e3) / 1e9) / peak,
+                         "dominant_phase": dom},
+            "phases": phase_out,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gen_seconds": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,176 @@
+/*
+ * prost_b200.h — C-ABI of the B200-native pROST per-frame step.
+ *
+ * One shared library (paper_1302_2073_b200/_lib/libprost_b200.so) exports
+ * exactly these symbols.  No C++ or torch types cross the boundary: plain
+ * pointers, sizes and POD structs.  The reference is pure Python (no FFI of
+ * its own); each entry point below names the reference interface it
+ * replaces, paths relative to /root/reference/pkg/src/prost/.
+ *
+ *   prost_create / prost_destroy
+ *       StreamTracker(RunConfig) construction, jobs.py:161-171, and
+ *       bootstrap(), tracker.py:106-118 (the basis itself is drawn on the
+ *       host with numpy exactly as manifold.py:100-113 and handed over with
+ *       prost_set_core_state, so U0 is bit-identical to the reference's).
+ *   prost_push
+ *       StreamTracker.push(FrameBuffer) -> FrameRecord, jobs.py:186-229
+ *       (PROST_FLAG_PIPELINE), or process_frame(state, x, params),
+ *       tracker.py:121-156 (no PIPELINE flag: x is already normalized, the
+ *       residual against U' is returned and weights stay per coordinate).
+ *   prost_background
+ *       StreamTracker.background_frame(), jobs.py:231-239.
+ *   prost_set_core_state / prost_get_core_state
+ *       TrackerState(basis, y, weights, frame_index) of tracker.py:79-87
+ *       and SubspaceBasis.steps_since_qr, manifold.py:49-78.
+ *   prost_set_preproc / prost_get_preproc
+ *       PreprocStats, pipeline.py:99-161 (and the snapshot fields of
+ *       tracker.py:184-209).
+ *
+ * Status codes map one-to-one onto the reference's error classes
+ * (errors.py:14-39); the Python host raises the matching class.
+ *
+ * Threading: a handle is single-owner (tracker.py:10-11, jobs.py:157-158);
+ * calls are enqueued on the caller's CUDA stream (NULL = legacy default).
+ */
+#ifndef PROST_B200_H
+#define PROST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PROST_ABI_VERSION 1
+
+/* status codes (errors.py:14-39) */
+#define PROST_OK 0
+#define PROST_ERR_CONFIG 1      /* ConfigError    */
+#define PROST_ERR_DIMENSION 2   /* DimensionError */
+#define PROST_ERR_NONFINITE 3   /* NonFiniteError */
+#define PROST_ERR_SEQUENCE 4    /* SequenceError  */
+#define PROST_ERR_CUDA 5        /* device / driver failure (no reference analogue) */
+
+/* element types of frame / output buffers */
+#define PROST_F32 0
+#define PROST_F64 1
+#define PROST_U8 2   /* 8-bit intensities, divided by 255 on load (frameio.py:136) */
+
+/* handle flags */
+#define PROST_FLAG_PIPELINE 1u  /* StreamTracker semantics: running-stats normalization,
+                                   threshold (segment), 3x3 median, per-pixel weights */
+#define PROST_FLAG_FP64 2u      /* double-precision state and per-element arithmetic
+                                   (parity instantiation); default is fp32 */
+
+/* Tracker tunables: ProstParams (tracker.py:45-76) + LpConfig (cost.py:29-45)
+ * + CgOptions (fit.py:24-47) + the RunConfig fields the pipeline needs
+ * (jobs.py:74-120).  mu and tau must already be resolved. */
+typedef struct prost_params {
+  int32_t k;              /* subspace dimension, 1 <= k <= 32, k < n */
+  int32_t width;          /* pixels per row */
+  int32_t height;         /* rows */
+  int32_t channels;       /* 1 or 3, channel-planar (pipeline.py:1-6) */
+  int32_t cg_max_iters;   /* CgOptions.max_iters (>= 1) */
+  int32_t max_backtracks; /* CgOptions.max_backtracks (1..64) */
+  int32_t i_init;         /* statistics window (jobs.py:71) */
+  int32_t reserved;
+  double p, mu, delta, omega, t_init, t_min, tau;
+  double grad_tol, initial_step, shrink, sufficient_decrease;
+} prost_params;
+
+/* FitResult (fit.py:50-63) + FrameRecord scalars (jobs.py:142-151). */
+typedef struct prost_fit_info {
+  double fit_cost;        /* FitResult.cost / FrameRecord.fit_cost */
+  double step;            /* step_size(frame_index) used by this frame */
+  int64_t frame_index;    /* after the step (FrameRecord.frame_index) */
+  int32_t iterations, cost_evals, grad_evals;
+  int32_t status;         /* PROST_OK or PROST_ERR_NONFINITE for this stream */
+} prost_fit_info;
+
+/* Per-push outputs; every pointer may be NULL.  Arrays are stream-major:
+ * background/residual [n_streams][n], masks [n_streams][width*height]. */
+typedef struct prost_outputs {
+  void* background;       /* clip(U'y*std + mean, 0, 1): background_frame() after the push */
+  void* residual;         /* x - U'y in the normalized domain (FrameRecord.residual) */
+  uint8_t* mask;          /* median3x3(raw_mask) (FrameRecord.mask) */
+  uint8_t* raw_mask;      /* segment(residual) (FrameRecord.raw_mask) */
+  prost_fit_info* fit;    /* HOST array [n_streams]; non-NULL makes the call synchronous */
+  int32_t dtype;          /* PROST_F32 or PROST_F64 for background/residual */
+  int32_t on_device;      /* 1: the array pointers above are device pointers */
+} prost_outputs;
+
+typedef struct prost_handle prost_handle;
+
+int prost_abi_version(void);
+
+/* n_streams independent trackers sharing one parameter set, batched in every
+ * launch.  device: CUDA ordinal.  Bases start as the first k unit vectors;
+ * call prost_set_core_state per stream with the numpy-drawn basis. */
+int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags,
+                 int32_t device, prost_handle** out);
+void prost_destroy(prost_handle* h);
+
+/* U: host [n][k] row-major f64 (SubspaceBasis.data), y: [k], weights: [n]
+ * with values in {1, omega} (per coordinate; in pipeline mode all channels of
+ * a pixel must agree).  Any pointer may be NULL to leave that field. */
+int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const double* y,
+                         const double* weights, int64_t frame_index, int64_t steps_since_qr);
+int prost_get_core_state(prost_handle* h, int32_t stream, double* U, double* y,
+                         double* weights, int64_t* frame_index, int64_t* steps_since_qr);
+
+/* mean: [n]; scalars: [value_sum, value_sumsq, value_count, frames_seen, frozen, std]
+ * (pipeline.py:99-118). */
+int prost_set_preproc(prost_handle* h, int32_t stream, const double* mean, const double* scalars);
+int prost_get_preproc(prost_handle* h, int32_t stream, double* mean, double* scalars);
+
+/* One frame for every stream: frames [n_streams][n] of `dtype`, host or
+ * device memory.  Pipeline mode: raw intensities in [0,1] (or u8).  Core mode:
+ * the already-normalized vector x of process_frame. */
+int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
+               const prost_outputs* out, void* cuda_stream);
+
+/* background_frame() for every stream into out [n_streams][n] (pipeline mode). */
+int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_device,
+                     void* cuda_stream);
+
+/* Wait for all work enqueued by this handle; returns the first per-stream
+ * status of the last push (PROST_ERR_NONFINITE if a frame was rejected). */
+int prost_synchronize(prost_handle* h);
+
+/* Copy the last error message into buf (NUL-terminated); returns its length. */
+int prost_last_error(prost_handle* h, char* buf, int32_t len);
+
+/* Introspection: PROST_Q_LAUNCHES (kernel launches so far), PROST_Q_WAVE
+ * (streams per launch wave), PROST_Q_BYTES_U (bytes of U per stream),
+ * PROST_Q_CHUNKS (CTAs per stream per launch). */
+#define PROST_Q_LAUNCHES 0
+#define PROST_Q_WAVE 1
+#define PROST_Q_BYTES_U 2
+#define PROST_Q_CHUNKS 3
+#define PROST_Q_INSTANCE_K 4
+int prost_query(prost_handle* h, int32_t what, int64_t* value);
+
+/* Per-phase device timing (CUDA events around every launch, on the launch
+ * stream).  prost_profile_read returns and resets the accumulated milliseconds
+ * and launch counts per phase, indexed by PROST_PH_*. */
+#define PROST_PH_STATS 0
+#define PROST_PH_COLD 1
+#define PROST_PH_PASS0 2
+#define PROST_PH_ITER 3
+#define PROST_PH_LSFB 4
+#define PROST_PH_GRADFB 5
+#define PROST_PH_GEO 6
+#define PROST_PH_QR 7
+#define PROST_PH_MEDIAN 8
+#define PROST_N_PHASES 9
+int prost_profile(prost_handle* h, int32_t enable);
+int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n_phases);
+
+/* Tuning knob: streams per launch wave (0 = automatic, sized to L2). */
+int prost_set_wave(prost_handle* h, int32_t streams_per_wave);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PROST_B200_H */

@@ -1,0 +1,775 @@
+// prost_b200.cu — host side of the C-ABI declared in include/prost_b200.h.
+//
+// A handle owns the device state of n_streams trackers (basis planes, labels,
+// running statistics, control blocks) and enqueues one frame as a fixed
+// sequence of phase kernels (prost_phases.cuh) on the caller's CUDA stream.
+// Data-dependent control flow (Armijo fallbacks, periodic QR, first-frame
+// cold start) is decided on the device: kernels whose condition is false for
+// a stream exit immediately, so the host never synchronizes inside a frame.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/prost_b200.h"
+#include "prost_phases.cuh"
+
+using namespace prost;
+
+static_assert(sizeof(FitInfo) == sizeof(prost_fit_info), "FitInfo layout");
+
+namespace {
+
+struct Ops {
+  void (*frame)(prost_handle*, Args&, cudaStream_t, int sw);
+  void (*background)(prost_handle*, Args&, cudaStream_t, int sw);
+  int K, VEC;
+};
+
+}  // namespace
+
+struct prost_handle {
+  prost_params prm;
+  int S = 0;
+  uint32_t flags = 0;
+  int device = 0;
+  bool fp64 = false, pipeline = false;
+  int k = 0, C = 1, P = 0, Pp = 0;
+  long long np = 0;
+  size_t esz = 4;
+  int chunks = 1, nvmax = 0, wave = 0, n_ls = 0;
+  Ops ops{};
+  // device state
+  void* U = nullptr;
+  void* r = nullptr;
+  void* ud = nullptr;
+  void* x = nullptr;
+  void* mean = nullptr;
+  uint8_t* lab = nullptr;
+  Ctl* ctl = nullptr;
+  double* part = nullptr;
+  unsigned* cnt = nullptr;
+  double* rinv = nullptr;
+  FitInfo* info = nullptr;
+  FitInfo* info_h = nullptr;  // pinned
+  // lazily allocated
+  void* bgbuf = nullptr;
+  void* resbuf = nullptr;
+  uint8_t* maskbuf = nullptr;
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  long long launches = 0;
+  bool maybe_cold = true;
+  // optional per-phase timing (prost_profile)
+  bool prof = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[PROST_N_PHASES] = {0};
+  long long prof_n[PROST_N_PHASES] = {0};
+  std::string err;
+};
+
+namespace {
+
+int fail(prost_handle* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(h, PROST_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                \
+  } while (0)
+
+inline int blocks_for(long long n, int t = NT) {
+  long long b = (n + t - 1) / t;
+  return (int)std::min<long long>(std::max<long long>(b, 1), 148LL * 16);
+}
+
+Args make_args(prost_handle* h, int s0) {
+  Args a;
+  std::memset(&a, 0, sizeof a);
+  a.U = h->U;
+  a.r = h->r;
+  a.ud = h->ud;
+  a.x = h->x;
+  a.mean = h->mean;
+  a.lab = h->lab;
+  a.ctl = h->ctl;
+  a.part = h->part;
+  a.cnt = h->cnt;
+  a.rinv = h->rinv;
+  a.info = h->info;
+  a.s0 = s0;
+  a.k = h->k;
+  a.C = h->C;
+  a.P = h->P;
+  a.Pp = h->Pp;
+  a.width = h->prm.width;
+  a.height = h->prm.height;
+  a.np = h->np;
+  a.chunks = h->chunks;
+  a.nvmax = h->nvmax;
+  a.pipeline = h->pipeline ? 1 : 0;
+  a.max_iters = h->prm.cg_max_iters;
+  a.max_bt = h->prm.max_backtracks;
+  a.i_init = h->prm.i_init;
+  const double p = h->prm.p;
+  a.pmode = p == 2.0 ? PM_TWO : (p == 1.0 ? PM_ONE : ((p == 0.5 && !h->fp64) ? PM_HALF : PM_GENERAL));
+  a.n_real = h->C * h->P;
+  a.p = p;
+  a.half_p = 0.5 * p;
+  a.mu = h->prm.mu;
+  a.delta = h->prm.delta;
+  a.omega = h->prm.omega;
+  a.t_init = h->prm.t_init;
+  a.t_min = h->prm.t_min;
+  a.tau = h->prm.tau;
+  a.grad_tol = h->prm.grad_tol;
+  a.step0 = h->prm.initial_step;
+  a.shrink = h->prm.shrink;
+  a.c_armijo = h->prm.sufficient_decrease;
+  return a;
+}
+
+cudaEvent_t take_event(prost_handle* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Records a CUDA event pair around one kernel launch when profiling is on.
+struct PhaseTimer {
+  prost_handle* h;
+  cudaStream_t st;
+  int phase;
+  cudaEvent_t e0 = nullptr;
+  PhaseTimer(prost_handle* h_, cudaStream_t st_, int ph) : h(h_), st(st_), phase(ph) {
+    if (h->prof) {
+      e0 = take_event(h);
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~PhaseTimer() {
+    if (h->prof) {
+      cudaEvent_t e1 = take_event(h);
+      cudaEventRecord(e1, st);
+      h->prof_ev.push_back({phase, {e0, e1}});
+    }
+  }
+};
+
+#define LAUNCH(phase, ...)                  \
+  do {                                      \
+    PhaseTimer pt_(h, st, phase);           \
+    __VA_ARGS__;                            \
+    ++n;                                    \
+  } while (0)
+
+template <typename T, int K>
+struct Impl {
+  static constexpr int VEC = Vec<T, K>::value;
+
+  static void frame(prost_handle* h, Args& a, cudaStream_t st, int sw) {
+    const dim3 grid(h->chunks, sw);
+    long long n = 0;
+    LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a)));
+    if (h->maybe_cold) LAUNCH(PROST_PH_COLD, (k_cold<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    LAUNCH(PROST_PH_PASS0, (k_pass0<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    for (int it = 0; it < h->prm.cg_max_iters; ++it) {
+      LAUNCH(PROST_PH_ITER, (k_iter<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+      for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
+      LAUNCH(PROST_PH_GRADFB, (k_gradfb<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    }
+    LAUNCH(PROST_PH_GEO, (k_geo<T, K, VEC, false><<<grid, NT, 0, st>>>(a)));
+    LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
+    if (a.mask_out) {
+      const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), sw);
+      LAUNCH(PROST_PH_MEDIAN, (k_median<<<mg, NT, 0, st>>>(a)));
+    }
+    h->launches += n;
+  }
+
+  static void background(prost_handle* h, Args& a, cudaStream_t st, int sw) {
+    k_background<T, K, VEC><<<dim3(h->chunks, sw), NT, 0, st>>>(a);
+    h->launches += 1;
+  }
+};
+
+template <typename T>
+Ops pick(int k) {
+#define PROST_K(KK) \
+  if (k <= KK) return Ops{&Impl<T, KK>::frame, &Impl<T, KK>::background, KK, Impl<T, KK>::VEC};
+  PROST_K(4)
+  PROST_K(8)
+  PROST_K(15)
+  PROST_K(16)
+  PROST_K(20)
+  PROST_K(30)
+  PROST_K(32)
+#undef PROST_K
+  return Ops{nullptr, nullptr, 0, 0};
+}
+
+int validate(prost_handle* h, const prost_params* p, int n_streams) {
+  // The reference's own checks (tracker.py:64-76, cost.py:41-45, fit.py:35-47)
+  // plus the limits of this implementation.
+  if (p->k < 1) return fail(h, PROST_ERR_CONFIG, "subspace dimension must be >= 1, got %d", p->k);
+  if (!(p->p > 0.0 && p->p <= 2.0)) return fail(h, PROST_ERR_CONFIG, "p must be in (0, 2], got %g", p->p);
+  if (!(p->mu > 0.0)) return fail(h, PROST_ERR_CONFIG, "mu must be > 0, got %g", p->mu);
+  if (!(p->delta > 0.0)) return fail(h, PROST_ERR_CONFIG, "delta must be > 0, got %g", p->delta);
+  if (!(p->omega > 0.0 && p->omega <= 1.0))
+    return fail(h, PROST_ERR_CONFIG, "omega must be in (0, 1], got %g", p->omega);
+  if (!(p->t_min > 0.0 && p->t_min <= p->t_init))
+    return fail(h, PROST_ERR_CONFIG, "need 0 < t_min <= t_init, got t_min=%g, t_init=%g", p->t_min, p->t_init);
+  if (!(p->tau >= 0.0)) return fail(h, PROST_ERR_CONFIG, "tau must be >= 0, got %g", p->tau);
+  if (p->cg_max_iters < 1) return fail(h, PROST_ERR_CONFIG, "max_iters must be >= 1, got %d", p->cg_max_iters);
+  if (!(p->grad_tol >= 0.0)) return fail(h, PROST_ERR_CONFIG, "grad_tol must be >= 0, got %g", p->grad_tol);
+  if (!(p->shrink > 0.0 && p->shrink < 1.0)) return fail(h, PROST_ERR_CONFIG, "shrink must be in (0, 1), got %g", p->shrink);
+  if (!(p->sufficient_decrease > 0.0 && p->sufficient_decrease <= 0.5))
+    return fail(h, PROST_ERR_CONFIG, "sufficient_decrease must be in (0, 0.5], got %g", p->sufficient_decrease);
+  if (p->max_backtracks < 1) return fail(h, PROST_ERR_CONFIG, "max_backtracks must be >= 1, got %d", p->max_backtracks);
+  if (p->max_backtracks > MAXBT) return fail(h, PROST_ERR_CONFIG, "max_backtracks > %d is not supported", MAXBT);
+  if (!(p->initial_step > 0.0)) return fail(h, PROST_ERR_CONFIG, "initial_step must be > 0");
+  if (p->i_init < 1) return fail(h, PROST_ERR_CONFIG, "i_init must be >= 1, got %d", p->i_init);
+  if (p->channels != 1 && p->channels != 3)
+    return fail(h, PROST_ERR_DIMENSION, "channels must be 1 or 3, got %d", p->channels);
+  if (p->width < 1 || p->height < 1) return fail(h, PROST_ERR_DIMENSION, "bad dimensions %dx%d", p->width, p->height);
+  const long long n = (long long)p->width * p->height * p->channels;
+  if (!(p->k < n)) return fail(h, PROST_ERR_DIMENSION, "need 1 <= k < m, got m=%lld, k=%d", n, p->k);
+  if (p->k > KMAX) return fail(h, PROST_ERR_CONFIG, "k=%d exceeds the supported maximum %d", p->k, KMAX);
+  if (n_streams < 1) return fail(h, PROST_ERR_CONFIG, "n_streams must be >= 1");
+  if ((long long)p->width * p->height >= (1LL << 30)) return fail(h, PROST_ERR_DIMENSION, "frame too large");
+  return PROST_OK;
+}
+
+void* dev_alloc(size_t bytes, cudaError_t* e) {
+  void* p = nullptr;
+  *e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+  if (*e == cudaSuccess) *e = cudaMemset(p, 0, std::max<size_t>(bytes, 16));
+  return p;
+}
+
+int ensure_stage(prost_handle* h, size_t bytes) {
+  if (h->stage_bytes >= bytes) return PROST_OK;
+  if (h->stage) cudaFree(h->stage);
+  h->stage = nullptr;
+  h->stage_bytes = 0;
+  CK(cudaMalloc(&h->stage, bytes));
+  h->stage_bytes = bytes;
+  return PROST_OK;
+}
+
+size_t dtype_size(int dt) { return dt == PROST_F64 ? 8 : (dt == PROST_U8 ? 1 : 4); }
+
+// Copy a dense [S][C][P] array of dtype `dt` (host or device) into a padded
+// device array of the handle's element type.
+int upload_dense(prost_handle* h, const void* src, int dt, int on_device, void* dst, int rows,
+                 cudaStream_t st) {
+  const int P = h->P, Pp = h->Pp;
+  const size_t dsz = dtype_size(dt);
+  const bool same = (dt == PROST_F64) == h->fp64 && dt != PROST_U8;
+  if (same) {
+    CK(cudaMemcpy2DAsync(dst, (size_t)Pp * h->esz, src, (size_t)P * dsz, (size_t)P * dsz, rows,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    return PROST_OK;
+  }
+  const void* dsrc = src;
+  if (!on_device) {
+    int rc = ensure_stage(h, (size_t)rows * P * dsz);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->stage, src, (size_t)rows * P * dsz, cudaMemcpyHostToDevice, st));
+    dsrc = h->stage;
+  }
+  const int nb = blocks_for((long long)rows * P);
+  const double sc = dt == PROST_U8 ? 1.0 / 255.0 : 1.0;
+  if (h->fp64) {
+    if (dt == PROST_F32) k_pack<float, double><<<nb, NT, 0, st>>>((const float*)dsrc, (double*)dst, rows, 1, P, Pp, 1, sc);
+    else k_pack<uint8_t, double><<<nb, NT, 0, st>>>((const uint8_t*)dsrc, (double*)dst, rows, 1, P, Pp, 1, sc);
+  } else {
+    if (dt == PROST_F64) k_pack<double, float><<<nb, NT, 0, st>>>((const double*)dsrc, (float*)dst, rows, 1, P, Pp, 1, sc);
+    else k_pack<uint8_t, float><<<nb, NT, 0, st>>>((const uint8_t*)dsrc, (float*)dst, rows, 1, P, Pp, 1, sc);
+  }
+  h->launches += 1;
+  CK(cudaGetLastError());
+  return PROST_OK;
+}
+
+// Copy a padded device array of the handle's element type into a dense user
+// array [rows][P] of dtype dt (host or device).
+int download_dense(prost_handle* h, const void* src, void* dst, int dt, int on_device, int rows,
+                   cudaStream_t st) {
+  const int P = h->P, Pp = h->Pp;
+  const size_t dsz = dtype_size(dt);
+  const bool same = (dt == PROST_F64) == h->fp64 && dt != PROST_U8;
+  if (same) {
+    CK(cudaMemcpy2DAsync(dst, (size_t)P * dsz, src, (size_t)Pp * h->esz, (size_t)P * dsz, rows,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    return PROST_OK;
+  }
+  if (dt == PROST_U8) return fail(h, PROST_ERR_CONFIG, "u8 is an input-only dtype");
+  void* ddst = dst;
+  if (!on_device) {
+    int rc = ensure_stage(h, (size_t)rows * P * dsz);
+    if (rc) return rc;
+    ddst = h->stage;
+  }
+  const int nb = blocks_for((long long)rows * P);
+  if (h->fp64) k_pack<double, float><<<nb, NT, 0, st>>>((const double*)src, (float*)ddst, rows, 1, P, Pp, 0, 1.0);
+  else k_pack<float, double><<<nb, NT, 0, st>>>((const float*)src, (double*)ddst, rows, 1, P, Pp, 0, 1.0);
+  h->launches += 1;
+  CK(cudaGetLastError());
+  if (!on_device) CK(cudaMemcpyAsync(dst, ddst, (size_t)rows * P * dsz, cudaMemcpyDeviceToHost, st));
+  return PROST_OK;
+}
+
+int copy_labels(prost_handle* h, const uint8_t* src, uint8_t* dst, int on_device, cudaStream_t st) {
+  CK(cudaMemcpy2DAsync(dst, h->P, src, h->Pp, h->P, h->S,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  return PROST_OK;
+}
+
+int check_stream(prost_handle* h, int s) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (s < 0 || s >= h->S) return fail(h, PROST_ERR_DIMENSION, "stream %d out of range [0, %d)", s, h->S);
+  return PROST_OK;
+}
+
+template <typename T>
+void rows_to_planes(const double* U, int n_rows_dense, int k, int C, int P, int Pp, std::vector<T>& out) {
+  // U row-major [C*P][k] -> planes [k][C*Pp]
+  const size_t np = (size_t)C * Pp;
+  out.assign((size_t)k * np, (T)0);
+  for (int c = 0; c < C; ++c)
+    for (int p = 0; p < P; ++p) {
+      const size_t row = (size_t)c * P + p;
+      for (int j = 0; j < k; ++j) out[(size_t)j * np + (size_t)c * Pp + p] = (T)U[row * k + j];
+    }
+  (void)n_rows_dense;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+int prost_abi_version(void) { return PROST_ABI_VERSION; }
+
+int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, int32_t device,
+                 prost_handle** out) {
+  if (!params || !out) return PROST_ERR_CONFIG;
+  *out = nullptr;
+  prost_handle* h = new prost_handle();
+  int rc = validate(h, params, n_streams);
+  if (rc) {
+    // keep the handle so the caller can read the message, then destroy it
+    *out = h;
+    return rc;
+  }
+  h->prm = *params;
+  h->S = n_streams;
+  h->flags = flags;
+  h->device = device;
+  h->fp64 = (flags & PROST_FLAG_FP64) != 0;
+  h->pipeline = (flags & PROST_FLAG_PIPELINE) != 0;
+  h->k = params->k;
+  h->C = params->channels;
+  h->P = params->width * params->height;
+  h->Pp = (h->P + 3) / 4 * 4;
+  h->np = (long long)h->C * h->Pp;
+  h->esz = h->fp64 ? 8 : 4;
+  h->ops = h->fp64 ? pick<double>(h->k) : pick<float>(h->k);
+  *out = h;
+  if (!h->ops.frame) return fail(h, PROST_ERR_CONFIG, "no kernel instance for k=%d", h->k);
+  const int K = h->ops.K;
+  h->nvmax = std::max({K + 3, WC + WG * (K + 1), LSW, K * (K + 1) / 2, 3});
+  h->n_ls = params->max_backtracks > WC ? (params->max_backtracks - WC + LSW - 1) / LSW : 0;
+  CK(cudaSetDevice(device));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const long long groups = (h->Pp / h->ops.VEC + NT - 1) / NT;
+  const long long target = (long long)sms * 8 * 2;
+  h->chunks = (int)std::max<long long>(1, std::min<long long>(groups, (target + h->S - 1) / h->S));
+  h->wave = h->S;
+  cudaError_t e = cudaSuccess;
+  const size_t S = h->S, np = h->np, esz = h->esz;
+#define ALLOC(field, bytes)                                                             \
+  do {                                                                                  \
+    h->field = (decltype(h->field))dev_alloc((bytes), &e);                              \
+    if (e != cudaSuccess)                                                               \
+      return fail(h, PROST_ERR_CUDA, "cudaMalloc(%s, %zu): %s", #field, (size_t)(bytes), \
+                  cudaGetErrorString(e));                                               \
+  } while (0)
+  ALLOC(U, S * h->k * np * esz);
+  ALLOC(r, S * np * esz);
+  ALLOC(ud, S * np * esz);
+  ALLOC(x, S * np * esz);
+  ALLOC(mean, S * np * esz);
+  ALLOC(lab, S * h->Pp);
+  ALLOC(ctl, S * sizeof(Ctl));
+  ALLOC(part, S * h->chunks * h->nvmax * sizeof(double));
+  ALLOC(cnt, S * sizeof(unsigned));
+  ALLOC(rinv, S * KMAX * KMAX * sizeof(double));
+  ALLOC(info, S * sizeof(FitInfo));
+#undef ALLOC
+  CK(cudaMallocHost(&h->info_h, S * sizeof(FitInfo)));
+  // U = first k unit vectors until the caller installs the numpy-drawn basis
+  if (h->fp64) {
+    std::vector<double> eye;
+    std::vector<double> Ud((size_t)h->C * h->P * h->k, 0.0);
+    for (int j = 0; j < h->k; ++j) Ud[(size_t)j * h->k + j] = 1.0;
+    rows_to_planes<double>(Ud.data(), 0, h->k, h->C, h->P, h->Pp, eye);
+    for (size_t s = 0; s < S; ++s)
+      CK(cudaMemcpy((char*)h->U + s * h->k * np * esz, eye.data(), eye.size() * esz, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> eye;
+    std::vector<double> Ud((size_t)h->C * h->P * h->k, 0.0);
+    for (int j = 0; j < h->k; ++j) Ud[(size_t)j * h->k + j] = 1.0;
+    rows_to_planes<float>(Ud.data(), 0, h->k, h->C, h->P, h->Pp, eye);
+    for (size_t s = 0; s < S; ++s)
+      CK(cudaMemcpy((char*)h->U + s * h->k * np * esz, eye.data(), eye.size() * esz, cudaMemcpyHostToDevice));
+  }
+  CK(cudaDeviceSynchronize());
+  return PROST_OK;
+}
+
+void prost_destroy(prost_handle* h) {
+  if (!h) return;
+  void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
+                  h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h->info_h) cudaFreeHost(h->info_h);
+  for (auto& pe : h->prof_ev) {
+    cudaEventDestroy(pe.second.first);
+    cudaEventDestroy(pe.second.second);
+  }
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  delete h;
+}
+
+int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const double* y,
+                         const double* weights, int64_t frame_index, int64_t steps_since_qr) {
+  int rc = check_stream(h, stream);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  const int k = h->k, C = h->C, P = h->P, Pp = h->Pp;
+  const size_t np = h->np;
+  if (U) {
+    if (h->fp64) {
+      std::vector<double> pl;
+      rows_to_planes<double>(U, 0, k, C, P, Pp, pl);
+      CK(cudaMemcpy((char*)h->U + (size_t)stream * k * np * h->esz, pl.data(), pl.size() * 8, cudaMemcpyHostToDevice));
+    } else {
+      std::vector<float> pl;
+      rows_to_planes<float>(U, 0, k, C, P, Pp, pl);
+      CK(cudaMemcpy((char*)h->U + (size_t)stream * k * np * h->esz, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  if (weights) {
+    std::vector<uint8_t> lb(Pp, 0);
+    for (int p = 0; p < P; ++p) {
+      for (int c = 0; c < C; ++c) {
+        const double w = weights[(size_t)c * P + p];
+        const uint8_t l = (w == 1.0) ? 0 : 1;
+        if (w != 1.0 && w != h->prm.omega)
+          return fail(h, PROST_ERR_CONFIG, "weights must be 1 or omega (%g), got %g", h->prm.omega, w);
+        if (c == 0) lb[p] = l;
+        else if (lb[p] != l)
+          return fail(h, PROST_ERR_CONFIG, "channel weights of pixel %d disagree", p);
+      }
+    }
+    CK(cudaMemcpy(h->lab + (size_t)stream * Pp, lb.data(), Pp, cudaMemcpyHostToDevice));
+  }
+  Ctl c;
+  CK(cudaMemcpy(&c, h->ctl + stream, sizeof c, cudaMemcpyDeviceToHost));
+  if (y)
+    for (int j = 0; j < k; ++j) c.y[j] = y[j];
+  c.frame_index = frame_index;
+  c.since_qr = steps_since_qr;
+  c.status = ST_OK;
+  c.active = 0;
+  CK(cudaMemcpy(h->ctl + stream, &c, sizeof c, cudaMemcpyHostToDevice));
+  if (frame_index == 0) h->maybe_cold = true;
+  return PROST_OK;
+}
+
+int prost_get_core_state(prost_handle* h, int32_t stream, double* U, double* y, double* weights,
+                         int64_t* frame_index, int64_t* steps_since_qr) {
+  int rc = check_stream(h, stream);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  const int k = h->k, C = h->C, P = h->P, Pp = h->Pp;
+  const size_t np = h->np;
+  if (U) {
+    std::vector<char> raw((size_t)k * np * h->esz);
+    CK(cudaMemcpy(raw.data(), (char*)h->U + (size_t)stream * k * np * h->esz, raw.size(), cudaMemcpyDeviceToHost));
+    for (int c = 0; c < C; ++c)
+      for (int p = 0; p < P; ++p)
+        for (int j = 0; j < k; ++j) {
+          const size_t src = (size_t)j * np + (size_t)c * Pp + p;
+          U[((size_t)c * P + p) * k + j] =
+              h->fp64 ? ((const double*)raw.data())[src] : (double)((const float*)raw.data())[src];
+        }
+  }
+  if (weights) {
+    std::vector<uint8_t> lb(Pp);
+    CK(cudaMemcpy(lb.data(), h->lab + (size_t)stream * Pp, Pp, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < C; ++c)
+      for (int p = 0; p < P; ++p) weights[(size_t)c * P + p] = lb[p] ? h->prm.omega : 1.0;
+  }
+  Ctl c;
+  CK(cudaMemcpy(&c, h->ctl + stream, sizeof c, cudaMemcpyDeviceToHost));
+  if (y)
+    for (int j = 0; j < k; ++j) y[j] = c.y[j];
+  if (frame_index) *frame_index = c.frame_index;
+  if (steps_since_qr) *steps_since_qr = c.since_qr;
+  return PROST_OK;
+}
+
+int prost_set_preproc(prost_handle* h, int32_t stream, const double* mean, const double* sc) {
+  int rc = check_stream(h, stream);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  if (mean) {
+    rc = upload_dense(h, mean, PROST_F64, 0, (char*)h->mean + (size_t)stream * h->np * h->esz, h->C, 0);
+    if (rc) return rc;
+    CK(cudaDeviceSynchronize());
+  }
+  if (sc) {
+    Ctl c;
+    CK(cudaMemcpy(&c, h->ctl + stream, sizeof c, cudaMemcpyDeviceToHost));
+    c.psum = sc[0];
+    c.psumsq = sc[1];
+    c.pcount = (long long)sc[2];
+    c.pseen = (long long)sc[3];
+    c.frozen = sc[4] != 0.0;
+    c.pstd = sc[5];
+    CK(cudaMemcpy(h->ctl + stream, &c, sizeof c, cudaMemcpyHostToDevice));
+  }
+  return PROST_OK;
+}
+
+int prost_get_preproc(prost_handle* h, int32_t stream, double* mean, double* sc) {
+  int rc = check_stream(h, stream);
+  if (rc) return rc;
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  if (mean) {
+    rc = download_dense(h, (char*)h->mean + (size_t)stream * h->np * h->esz, mean, PROST_F64, 0, h->C, 0);
+    if (rc) return rc;
+    CK(cudaDeviceSynchronize());
+  }
+  if (sc) {
+    Ctl c;
+    CK(cudaMemcpy(&c, h->ctl + stream, sizeof c, cudaMemcpyDeviceToHost));
+    sc[0] = c.psum;
+    sc[1] = c.psumsq;
+    sc[2] = (double)c.pcount;
+    sc[3] = (double)c.pseen;
+    sc[4] = c.frozen ? 1.0 : 0.0;
+    sc[5] = c.pstd;
+  }
+  return PROST_OK;
+}
+
+int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
+               const prost_outputs* out, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!frames) return fail(h, PROST_ERR_DIMENSION, "frames is NULL");
+  if (dtype != PROST_F32 && dtype != PROST_F64 && dtype != PROST_U8)
+    return fail(h, PROST_ERR_CONFIG, "unknown frame dtype %d", dtype);
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const bool same = (dtype == PROST_F64) == h->fp64 && dtype != PROST_U8;
+  const bool dense = h->P == h->Pp;
+  const void* xdev = h->x;
+  if (on_device && same && dense) {
+    xdev = frames;  // zero-copy: kernels read the caller's device frames
+  } else {
+    int rc = upload_dense(h, frames, dtype, on_device, h->x, h->S * h->C, st);
+    if (rc) return rc;
+  }
+  prost_outputs o{};
+  if (out) o = *out;
+  const int odt = o.dtype == PROST_F64 ? PROST_F64 : PROST_F32;
+  const bool osame = (odt == PROST_F64) == h->fp64;
+  const size_t fbytes = (size_t)h->S * h->np * h->esz;
+  cudaError_t e = cudaSuccess;
+  Args a = make_args(h, 0);
+  a.x = xdev;
+  if (o.background) {
+    if (o.on_device && osame && dense) a.bg_out = o.background;
+    else {
+      if (!h->bgbuf) h->bgbuf = dev_alloc(fbytes, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "bg buffer: %s", cudaGetErrorString(e));
+      a.bg_out = h->bgbuf;
+    }
+  }
+  if (o.residual) {
+    if (o.on_device && osame && dense) a.res_out = o.residual;
+    else {
+      if (!h->resbuf) h->resbuf = dev_alloc(fbytes, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "residual buffer: %s", cudaGetErrorString(e));
+      a.res_out = h->resbuf;
+    }
+  }
+  if (o.mask) {
+    if (o.on_device && dense) a.mask_out = o.mask;
+    else {
+      if (!h->maskbuf) h->maskbuf = (uint8_t*)dev_alloc((size_t)h->S * h->Pp, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "mask buffer: %s", cudaGetErrorString(e));
+      a.mask_out = h->maskbuf;
+    }
+  }
+  if (o.raw_mask && o.on_device && dense) a.raw_out = o.raw_mask;
+  const int wave = std::max(1, std::min(h->wave, h->S));
+  for (int s0 = 0; s0 < h->S; s0 += wave) {
+    a.s0 = s0;
+    h->ops.frame(h, a, st, std::min(wave, h->S - s0));
+  }
+  CK(cudaGetLastError());
+  h->maybe_cold = false;
+  // outputs the kernels could not write in place
+  int rc = PROST_OK;
+  if (o.background && a.bg_out == h->bgbuf)
+    rc = download_dense(h, h->bgbuf, o.background, odt, o.on_device, h->S * h->C, st);
+  if (!rc && o.residual && a.res_out == h->resbuf)
+    rc = download_dense(h, h->resbuf, o.residual, odt, o.on_device, h->S * h->C, st);
+  if (!rc && o.mask && a.mask_out == h->maskbuf) rc = copy_labels(h, h->maskbuf, o.mask, o.on_device, st);
+  if (!rc && o.raw_mask && a.raw_out == nullptr) rc = copy_labels(h, h->lab, o.raw_mask, o.on_device, st);
+  if (rc) return rc;
+  if (o.fit) {
+    CK(cudaMemcpyAsync(h->info_h, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(o.fit, h->info_h, (size_t)h->S * sizeof(FitInfo));
+    int first_bad = PROST_OK;
+    for (int s = 0; s < h->S; ++s) {
+      if (h->info_h[s].status != PROST_OK && first_bad == PROST_OK) first_bad = h->info_h[s].status;
+      if (h->info_h[s].status != PROST_OK && h->info_h[s].frame_index == 0) h->maybe_cold = true;
+    }
+    if (first_bad != PROST_OK) return fail(h, first_bad, "frame contains non-finite values");
+  }
+  return PROST_OK;
+}
+
+int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_device, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!out) return fail(h, PROST_ERR_DIMENSION, "out is NULL");
+  if (!h->pipeline) return fail(h, PROST_ERR_CONFIG, "background_frame needs a pipeline handle");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int odt = dtype == PROST_F64 ? PROST_F64 : PROST_F32;
+  const bool osame = (odt == PROST_F64) == h->fp64;
+  cudaError_t e = cudaSuccess;
+  Args a = make_args(h, 0);
+  if (on_device && osame && h->P == h->Pp) a.bg_out = out;
+  else {
+    if (!h->bgbuf) h->bgbuf = dev_alloc((size_t)h->S * h->np * h->esz, &e);
+    if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "bg buffer: %s", cudaGetErrorString(e));
+    a.bg_out = h->bgbuf;
+  }
+  h->ops.background(h, a, st, h->S);
+  CK(cudaGetLastError());
+  if (a.bg_out == h->bgbuf) {
+    int rc = download_dense(h, h->bgbuf, out, odt, on_device, h->S * h->C, st);
+    if (rc) return rc;
+  }
+  if (!on_device) CK(cudaStreamSynchronize(st));
+  return PROST_OK;
+}
+
+int prost_synchronize(prost_handle* h) {
+  if (!h) return PROST_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(h->info_h, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost));
+  for (int s = 0; s < h->S; ++s) {
+    if (h->info_h[s].status != PROST_OK) {
+      if (h->info_h[s].frame_index == 0) h->maybe_cold = true;
+      return fail(h, h->info_h[s].status, "stream %d: frame contains non-finite values", s);
+    }
+  }
+  return PROST_OK;
+}
+
+int prost_last_error(prost_handle* h, char* buf, int32_t len) {
+  if (!h || !buf || len <= 0) return 0;
+  const int n = (int)std::min<size_t>(h->err.size(), (size_t)len - 1);
+  std::memcpy(buf, h->err.data(), n);
+  buf[n] = 0;
+  return n;
+}
+
+int prost_query(prost_handle* h, int32_t what, int64_t* value) {
+  if (!h || !value) return PROST_ERR_CONFIG;
+  switch (what) {
+    case PROST_Q_LAUNCHES: *value = h->launches; break;
+    case PROST_Q_WAVE: *value = h->wave; break;
+    case PROST_Q_BYTES_U: *value = (int64_t)h->k * h->np * (int64_t)h->esz; break;
+    case PROST_Q_CHUNKS: *value = h->chunks; break;
+    case PROST_Q_INSTANCE_K: *value = h->ops.K; break;
+    default: return fail(h, PROST_ERR_CONFIG, "unknown query %d", what);
+  }
+  return PROST_OK;
+}
+
+int prost_profile(prost_handle* h, int32_t enable) {
+  if (!h) return PROST_ERR_CONFIG;
+  h->prof = enable != 0;
+  return PROST_OK;
+}
+
+int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n_phases) {
+  if (!h) return PROST_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
+  for (auto& pe : h->prof_ev) {
+    CK(cudaEventSynchronize(pe.second.second));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, pe.second.first, pe.second.second));
+    h->prof_ms[pe.first] += t;
+    h->prof_n[pe.first] += 1;
+    h->ev_pool.push_back(pe.second.first);
+    h->ev_pool.push_back(pe.second.second);
+  }
+  h->prof_ev.clear();
+  for (int i = 0; i < n_phases && i < PROST_N_PHASES; ++i) {
+    if (ms) ms[i] = h->prof_ms[i];
+    if (launches) launches[i] = h->prof_n[i];
+    h->prof_ms[i] = 0.0;
+    h->prof_n[i] = 0;
+  }
+  return PROST_OK;
+}
+
+int prost_set_wave(prost_handle* h, int32_t streams_per_wave) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (streams_per_wave < 0) return fail(h, PROST_ERR_CONFIG, "negative wave size");
+  h->wave = streams_per_wave == 0 ? h->S : streams_per_wave;
+  return PROST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,402 @@
+// prost_kernels.cuh — sm_100a kernels for the pROST per-frame step.
+//
+// The per-frame step (reference tracker.py:121-156) is a chain of dependent
+// global reductions over the n x k basis U.  Each phase below is one kernel
+// that streams U (stored as k coordinate planes of n_pad values per stream,
+// so every load is a coalesced 8/16-byte vector) over a grid of
+// (chunks, streams) CTAs.  Every CTA reduces its partial sums in a fixed
+// order, writes them to a slot, and the last CTA to arrive for a stream sums
+// the slots in slot order (deterministic, no float atomics) and runs the
+// scalar part of the algorithm for that stream in one warp (lane j owns
+// component j of the k-vectors), in double precision, writing the control
+// block that the next phase reads.
+//
+// Phases (host order, per frame):
+//   k_stats   running statistics of the raw frame (pipeline.py:120-140)
+//   k_cold    y = U^T x on the first frame (fit.py:86-87)
+//   k_pass0   r = x - U y, cost and coordinate gradient (fit.py:96-104)
+//   k_iter    u_dir = U d, Armijo trial costs for a window of WC step sizes
+//             and the coordinate gradient speculatively for WG of them
+//             (fit.py:108-144) — one U pass per CG iteration
+//   k_lsfb    remaining Armijo trials when the window held no acceptable step
+//             (elementwise over stored r and u_dir: no U traffic)
+//   k_gradfb  gradient at an accepted step outside the speculative window
+//   k_geo     rank-one geodesic update of U with the projected gradient,
+//             relabel, background and residual (manifold.py:116-197,
+//             tracker.py:140-147, jobs.py:231-239)
+//   k_gram / k_geo<QR>  periodic re-orthonormalization (manifold.py:192-196)
+//   k_median  3x3 majority filter (pipeline.py:215-228)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+namespace prost {
+
+constexpr int KMAX = 32;      // largest supported subspace dimension
+constexpr int NT = 256;       // threads per CTA
+constexpr int NW = NT / 32;   // warps per CTA
+constexpr int WC = 4;         // Armijo trial costs evaluated per U pass
+constexpr int WG = 2;         // speculative gradients per U pass
+constexpr int LSW = 16;       // trial costs per fallback line-search pass
+constexpr int MAXBT = 64;     // cap on CgOptions.max_backtracks
+constexpr int QR_EVERY = 1000;        // manifold.py:40
+constexpr double NORM_FLOOR = 1e-14;  // manifold.py:38
+constexpr double STD_FLOOR = 1e-6;    // pipeline.py:19
+
+enum PenaltyMode { PM_GENERAL = 0, PM_ONE = 1, PM_TWO = 2, PM_HALF = 3 };
+enum StreamStatus { ST_OK = 0, ST_NONFINITE = 3 };
+
+// Per-stream control block: everything the scalar part of the algorithm
+// carries between phases (double precision throughout).
+struct Ctl {
+  double y[KMAX], d[KMAX], grad[KMAX], v[KMAX];
+  double f;            // current cost (fit.py f_cur)
+  double slope;        // d . grad of the current iteration
+  double gnorm;        // ||grad|| at the start of the current iteration
+  double gsq;          // ||eta||^2 at the current residual
+  double pend_alpha;   // residual update r -= pend_alpha * u_dir not yet applied
+  double acc_alpha, acc_cost;
+  double std_cur;      // normalization scale of this frame
+  double t, geo_a, geo_s, geo_ln;
+  double psum, psumsq, pstd;
+  long long pcount, pseen, frame_index, since_qr;
+  int it, active, need_lsfb, need_gradfb, acc_idx, ls_next, gwin_lo, last_acc;
+  int do_geo, qr_now, status, iterations, cost_evals, grad_evals, frozen, cold;
+  int update_stats, pad_;
+};
+
+struct FitInfo {  // layout-identical to prost_fit_info
+  double fit_cost, step;
+  long long frame_index;
+  int iterations, cost_evals, grad_evals, status;
+};
+
+// Kernel arguments (passed by value; identical for every phase).
+struct Args {
+  void* U;             // [S][k][np]
+  void* r;             // [S][np] residual (lazily updated)
+  void* ud;            // [S][np] u_dir = U d of the last iteration
+  const void* x;       // [S][np] frame (raw intensities or normalized x)
+  void* mean;          // [S][np] running mean (pipeline)
+  uint8_t* lab;        // [S][Pp] labels: 1 = foreground (weight omega)
+  Ctl* ctl;            // [S]
+  double* part;        // [S][chunks][nvmax]
+  unsigned* cnt;       // [S]
+  double* rinv;        // [S][KMAX][KMAX] inverse Cholesky factor (periodic QR)
+  FitInfo* info;       // [S]
+  void* bg_out;        // [S][np] or null
+  void* res_out;       // [S][np] or null
+  uint8_t* raw_out;    // [S][Pp] or null
+  uint8_t* mask_out;   // [S][Pp] or null
+  int s0;              // first stream of this launch
+  int k, C, P, Pp, width, height;
+  long long np;        // padded coordinates per stream = C * Pp
+  int chunks, nvmax;
+  int pipeline, max_iters, max_bt, i_init, pmode, n_real;
+  double p, half_p, mu, delta, omega, t_init, t_min, tau, grad_tol, step0, shrink, c_armijo;
+};
+
+// ---------------------------------------------------------------------------
+// vector access: VEC consecutive coordinates of one plane
+
+template <typename T, int VEC> struct VecIO;
+
+template <> struct VecIO<float, 4> {
+  static __device__ __forceinline__ void ld(const float* p, float (&o)[4]) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  }
+  static __device__ __forceinline__ void ldg(const float* p, float (&o)[4]) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&o)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+};
+template <> struct VecIO<float, 2> {
+  static __device__ __forceinline__ void ld(const float* p, float (&o)[2]) {
+    float2 a = *reinterpret_cast<const float2*>(p);
+    o[0] = a.x; o[1] = a.y;
+  }
+  static __device__ __forceinline__ void ldg(const float* p, float (&o)[2]) {
+    float2 a = __ldg(reinterpret_cast<const float2*>(p));
+    o[0] = a.x; o[1] = a.y;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&o)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
+  }
+};
+template <> struct VecIO<double, 2> {
+  static __device__ __forceinline__ void ld(const double* p, double (&o)[2]) {
+    double2 a = *reinterpret_cast<const double2*>(p);
+    o[0] = a.x; o[1] = a.y;
+  }
+  static __device__ __forceinline__ void ldg(const double* p, double (&o)[2]) {
+    double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    o[0] = a.x; o[1] = a.y;
+  }
+  static __device__ __forceinline__ void st(double* p, const double (&o)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
+  }
+};
+template <> struct VecIO<double, 1> {
+  static __device__ __forceinline__ void ld(const double* p, double (&o)[1]) { o[0] = *p; }
+  static __device__ __forceinline__ void ldg(const double* p, double (&o)[1]) { o[0] = __ldg(p); }
+  static __device__ __forceinline__ void st(double* p, const double (&o)[1]) { *p = o[0]; }
+};
+
+template <int VEC> __device__ __forceinline__ void ld_lab(const uint8_t* p, uint8_t (&o)[VEC]) {
+  if constexpr (VEC == 4) {
+    uchar4 a = *reinterpret_cast<const uchar4*>(p);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  } else if constexpr (VEC == 2) {
+    uchar2 a = *reinterpret_cast<const uchar2*>(p);
+    o[0] = a.x; o[1] = a.y;
+  } else {
+    o[0] = *p;
+  }
+}
+template <int VEC> __device__ __forceinline__ void st_lab(uint8_t* p, const uint8_t (&o)[VEC]) {
+  if constexpr (VEC == 4) {
+    *reinterpret_cast<uchar4*>(p) = make_uchar4(o[0], o[1], o[2], o[3]);
+  } else if constexpr (VEC == 2) {
+    *reinterpret_cast<uchar2*>(p) = make_uchar2(o[0], o[1]);
+  } else {
+    *p = o[0];
+  }
+}
+
+// Coordinates per thread-vector: keeps the K*VEC basis values of one vector
+// group in at most ~64 registers.
+template <typename T, int K> struct Vec {
+  static constexpr int raw = 64 / (K * (int)(sizeof(T) / 4));
+  static constexpr int value = sizeof(T) == 8 ? (raw >= 2 ? 2 : 1) : (raw >= 4 ? 4 : 2);
+};
+
+// ---------------------------------------------------------------------------
+// smoothed lp penalty (cost.py:57-93): weighted term w*(r^2+mu)^(p/2) and the
+// residual gradient p*r*(w*term)/base.
+
+__device__ __forceinline__ void penalty(float r, float w, const Args& a, float& tw, float& g) {
+  const float b = fmaf(r, r, (float)a.mu);
+  switch (a.pmode) {
+    case PM_HALF: {  // b^(1/4) and b^(-3/4) from two MUFU.RSQ
+      const float h = rsqrtf(b);
+      const float e = rsqrtf(h);
+      tw = e * w;
+      g = (float)a.p * r * tw * (h * h);
+    } break;
+    case PM_ONE: {
+      const float h = rsqrtf(b);
+      tw = b * h * w;
+      g = (float)a.p * r * w * h;
+    } break;
+    case PM_TWO:
+      tw = b * w;
+      g = (float)a.p * r * w;
+      break;
+    default: {
+      const float L = __log2f(b);
+      tw = exp2f((float)a.half_p * L) * w;
+      g = (float)a.p * r * tw * __frcp_rn(b);
+    } break;
+  }
+}
+
+// Double instantiation: the same operation sequence and rounding as the
+// reference's numpy code (no FMA contraction), for 1e-10 parity.
+__device__ __forceinline__ void penalty(double r, double w, const Args& a, double& tw, double& g) {
+  const double b = __dadd_rn(__dmul_rn(r, r), a.mu);
+  double term;
+  if (a.pmode == PM_TWO) term = b;
+  else if (a.pmode == PM_ONE) term = sqrt(b);
+  else term = exp(__dmul_rn(a.half_p, log(b)));
+  tw = __dmul_rn(term, w);
+  g = __dmul_rn(__dmul_rn(a.p, r), __ddiv_rn(tw, b));
+}
+
+__device__ __forceinline__ float trial(float r, float al, float ud) { return fmaf(-al, ud, r); }
+__device__ __forceinline__ double trial(double r, double al, double ud) {
+  return __dsub_rn(r, __dmul_rn(al, ud));
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
+  return x;
+}
+
+// Reduce one per-thread value over the CTA into sm[warp][slot] (lane 0 writes).
+__device__ __forceinline__ void cta_stage(double x, double* sm, int slot, int nv) {
+  x = warp_sum(x);
+  if ((threadIdx.x & 31) == 0) sm[(threadIdx.x >> 5) * nv + slot] = x;
+}
+
+// Finish the CTA reduction: sum warps in order into this CTA's partial slot,
+// then arrive; returns true in the last CTA of the stream, whose `red` holds
+// the stream-wide sums (slots summed in slot order).
+__device__ __forceinline__ bool cta_finish(const Args& a, int s, double* sm, int nv, double* red) {
+  __shared__ int last;
+  double* slot = a.part + ((size_t)s * a.chunks + blockIdx.x) * a.nvmax;
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += NT) {
+    double acc = 0.0;
+    for (int w = 0; w < NW; ++w) acc += sm[w * nv + v];
+    slot[v] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev = atomicAdd(a.cnt + s, 1u);
+    last = (prev == (unsigned)(a.chunks - 1));
+    if (last) a.cnt[s] = 0u;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  const double* base = a.part + (size_t)s * a.chunks * a.nvmax;
+  for (int v = threadIdx.x; v < nv; v += NT) {
+    double acc = 0.0;
+    for (int c = 0; c < a.chunks; ++c) acc += __ldcg(base + (size_t)c * a.nvmax + v);
+    red[v] = acc;
+  }
+  __syncthreads();
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// scalar part of the algorithm (warp 0 of the last CTA; lane j owns j)
+
+__device__ __forceinline__ double step_size(const Args& a, long long i) {
+  // tracker.py:99-103
+  return fmax(exp(-a.tau * (double)i) * a.t_init, a.t_min);
+}
+
+__device__ __forceinline__ double alpha_at(const Args& a, int m) {
+  // fit.py:124,134: alpha *= shrink, starting from initial_step
+  double al = a.step0;
+  for (int i = 0; i < m; ++i) al *= a.shrink;
+  return al;
+}
+
+__device__ void write_info(Ctl* c, const Args& a, int s) {
+  FitInfo fi;
+  fi.fit_cost = c->f;
+  fi.step = c->t;
+  fi.frame_index = c->frame_index;
+  fi.iterations = c->iterations;
+  fi.cost_evals = c->cost_evals;
+  fi.grad_evals = c->grad_evals;
+  fi.status = c->status;
+  a.info[s] = fi;
+}
+
+// End of the CG loop: projected-gradient norm, geodesic scalars
+// (manifold.py:130-197, tracker.py:140-143).
+__device__ void finish_frame(Ctl* c, const Args& a, int s, int lane) {
+  const double t = step_size(a, c->frame_index);
+  const double gj = lane < a.k ? c->grad[lane] : 0.0;  // = U^T eta
+  const double yj = lane < a.k ? c->y[lane] : 0.0;
+  const double g2 = warp_sum(gj * gj);
+  const double rn = sqrt(warp_sum(yj * yj));
+  // ||eta - U U^T eta||^2 = ||eta||^2 - ||U^T eta||^2 for orthonormal U
+  const double ln = sqrt(fmax(c->gsq - g2, 0.0));
+  const bool zero = (ln < NORM_FLOOR) || (rn < NORM_FLOOR) || (t == 0.0);
+  if (!zero && lane < a.k) c->v[lane] = yj / rn;
+  __syncwarp();
+  if (lane == 0) {
+    c->active = 0;
+    c->t = t;
+    if (zero) {
+      c->do_geo = 0;
+      c->qr_now = 0;
+    } else {
+      const double phi = (ln * rn) * t;
+      c->do_geo = 1;
+      c->geo_a = cos(phi) - 1.0;
+      c->geo_s = sin(phi);
+      c->geo_ln = ln;
+      c->since_qr += 1;
+      c->qr_now = c->since_qr >= QR_EVERY ? 1 : 0;
+    }
+    c->frame_index += 1;
+    write_info(c, a, s);
+  }
+  __syncwarp();
+}
+
+// Top of CG iteration c->it (fit.py:108-119).
+__device__ void begin_iteration(Ctl* c, const Args& a, int s, int lane) {
+  if (lane == 0) {
+    c->need_lsfb = 0;
+    c->need_gradfb = 0;
+  }
+  __syncwarp();
+  if (c->it >= a.max_iters) { finish_frame(c, a, s, lane); return; }
+  const double gj = lane < a.k ? c->grad[lane] : 0.0;
+  const double gn = sqrt(warp_sum(gj * gj));
+  if (gn <= a.grad_tol) { finish_frame(c, a, s, lane); return; }
+  double dj = lane < a.k ? c->d[lane] : 0.0;
+  if (c->it > 0 && c->it % a.k == 0) dj = -gj;
+  double slope = warp_sum(dj * gj);
+  if (slope >= 0.0) {
+    dj = -gj;
+    slope = -gn * gn;
+  }
+  __syncwarp();
+  if (lane < a.k) c->d[lane] = dj;
+  __syncwarp();
+  if (lane == 0) {
+    c->slope = slope;
+    c->gnorm = gn;
+    c->active = 1;
+    int lo = c->last_acc;
+    lo = lo < 0 ? 0 : (lo > WC - WG ? WC - WG : lo);
+    c->gwin_lo = lo;
+  }
+  __syncwarp();
+}
+
+// Accepted step alpha with cost fnew and coordinate-gradient sums gs[j]
+// (= sum_i U_ij g_i): fit.py:137-144.
+__device__ void complete_iteration(Ctl* c, const Args& a, int s, int lane, double alpha,
+                                   double fnew, const double* gs, double gsq_new) {
+  const double dj = lane < a.k ? c->d[lane] : 0.0;
+  const double gold = lane < a.k ? c->grad[lane] : 0.0;
+  const double gnew = lane < a.k ? -gs[lane] : 0.0;
+  const double num = warp_sum(gnew * (gnew - gold));
+  const double beta = fmax(0.0, num / (c->gnorm * c->gnorm));
+  __syncwarp();
+  if (lane < a.k) {
+    c->y[lane] = c->y[lane] + alpha * dj;
+    c->d[lane] = -gnew + beta * dj;
+    c->grad[lane] = gnew;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    c->pend_alpha = alpha;
+    c->f = fnew;
+    c->gsq = gsq_new;
+    c->cost_evals += 1;
+    c->grad_evals += 1;
+    c->iterations = c->it + 1;
+    c->it += 1;
+  }
+  __syncwarp();
+  begin_iteration(c, a, s, lane);
+}
+
+__device__ void fail_iteration(Ctl* c, const Args& a, int s, int lane) {
+  // fit.py:133-134: no acceptable step -> leave the loop, residual unchanged
+  if (lane == 0) c->pend_alpha = 0.0;
+  __syncwarp();
+  finish_frame(c, a, s, lane);
+}
+
+}  // namespace prost

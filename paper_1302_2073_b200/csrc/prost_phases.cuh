@@ -1,0 +1,929 @@
+// prost_phases.cuh — the phase kernels of one tracker frame (see
+// prost_kernels.cuh for the overall structure).  Templated on the element type
+// T (float: the product path; double: the parity instantiation), the compiled
+// subspace bound K (runtime k <= K) and the coordinates-per-thread VEC.
+#pragma once
+
+#include "prost_kernels.cuh"
+
+namespace prost {
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_weights(const Args& a, const uint8_t* lab, int pix,
+                                             T (&w)[VEC]) {
+  uint8_t l[VEC];
+  ld_lab<VEC>(lab + pix, l);
+#pragma unroll
+  for (int e = 0; e < VEC; ++e)
+    w[e] = (pix + e < a.P) ? (l[e] ? (T)a.omega : (T)1) : (T)0;
+}
+
+__device__ __forceinline__ float norm_div(float x, float s) { return __fdiv_rn(x, s); }
+__device__ __forceinline__ double norm_div(double x, double s) { return __ddiv_rn(x, s); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// Normalized frame coordinates (pipeline.py:148-156; mean update 120-132).
+// `upd`: this frame folds into the running mean (frames_seen = `seen`);
+// `wr`: write the updated mean back.
+template <typename T, int VEC>
+__device__ __forceinline__ void normalized(const Args& a, size_t off, bool upd, bool wr, T seen,
+                                           T stdv, T (&xh)[VEC], bool& bad) {
+  const T* X = static_cast<const T*>(a.x) + off;
+  T xv[VEC];
+  VecIO<T, VEC>::ldg(X, xv);
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) bad |= !isfinite(xv[e]);
+  if (!a.pipeline) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) xh[e] = xv[e];
+    return;
+  }
+  T* M = static_cast<T*>(a.mean) + off;
+  T mv[VEC];
+  VecIO<T, VEC>::ld(M, mv);
+  if (upd) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) mv[e] = add_rn(mv[e], norm_div(sub_rn(xv[e], mv[e]), seen));
+    if (wr) VecIO<T, VEC>::st(M, mv);
+  }
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) xh[e] = norm_div(sub_rn(xv[e], mv[e]), stdv);
+}
+
+__device__ __forceinline__ double running_std(const Ctl* c) {
+  // pipeline.py:134-140
+  if (c->pcount < 2) return STD_FLOOR;
+  const double cnt = (double)c->pcount;
+  const double var = (c->psumsq - c->psum * c->psum / cnt) / (cnt - 1.0);
+  return fmax(sqrt(fmax(var, 0.0)), STD_FLOOR);
+}
+
+// ---------------------------------------------------------------------------
+// k_stats: frame start.  Pipeline frames inside the statistics window fold the
+// raw frame's sums into the running statistics (pipeline.py:120-132) and
+// reject non-finite frames; every other frame only fixes the normalization
+// scale (freezing it at frame i_init, jobs.py:201-209).
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_stats(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  const bool upd = a.pipeline && !c->frozen && c->frame_index < a.i_init;
+  if (!upd) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double sd = 1.0;
+      if (a.pipeline) {
+        sd = c->frozen ? c->pstd : running_std(c);
+        if (!c->frozen) {
+          c->frozen = 1;
+          c->pstd = sd;
+        }
+      }
+      c->std_cur = sd;
+      c->update_stats = 0;
+      c->status = ST_OK;
+    }
+    return;
+  }
+  __shared__ double sm[NW * 3];
+  __shared__ double red[3];
+  double s1 = 0.0, s2 = 0.0, nf = 0.0;
+  const int ng = a.Pp / VEC;
+  const T* X = static_cast<const T*>(a.x) + (size_t)s * a.np;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    for (int ch = 0; ch < a.C; ++ch) {
+      T xv[VEC];
+      VecIO<T, VEC>::ldg(X + (size_t)ch * a.Pp + pix, xv);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        if (pix + e < a.P) {
+          const double v = (double)xv[e];
+          s1 += v;
+          s2 += v * v;
+          nf += isfinite(v) ? 0.0 : 1.0;
+        }
+      }
+    }
+  }
+  cta_stage(s1, sm, 0, 3);
+  cta_stage(s2, sm, 1, 3);
+  cta_stage(nf, sm, 2, 3);
+  if (!cta_finish(a, s, sm, 3, red)) return;
+  if (threadIdx.x == 0) {
+    if (red[2] > 0.0) {
+      c->status = ST_NONFINITE;
+      c->t = step_size(a, c->frame_index);
+      write_info(c, a, s);
+    } else {
+      c->psum += red[0];
+      c->psumsq += red[1];
+      c->pcount += a.n_real;
+      c->pseen += 1;
+      c->std_cur = running_std(c);
+      c->update_stats = 1;
+      c->status = ST_OK;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_cold: y = U^T x on a stream's first frame (fit.py:86-87, tracker.py:136).
+
+template <typename T, int K, int VEC>
+__global__ void __launch_bounds__(NT) k_cold(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go, upd;
+  __shared__ double sstd, sseen;
+  if (threadIdx.x == 0) {
+    go = c->status == ST_OK && c->frame_index == 0;
+    upd = c->update_stats;
+    sstd = c->std_cur;
+    sseen = (double)c->pseen;
+  }
+  __syncthreads();
+  if (!go) return;
+  __shared__ double sm[NW * (K + 1)];
+  __shared__ double red[K + 1];
+  T acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) acc[j] = (T)0;
+  bool bad = false;
+  const int ng = a.Pp / VEC;
+  const T* U = static_cast<const T*>(a.U) + (size_t)s * a.k * a.np;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T xh[VEC];
+      normalized<T, VEC>(a, (size_t)s * a.np + off, upd, false, (T)sseen, (T)sstd, xh, bad);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (pix + e >= a.P) xh[e] = (T)0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < a.k) {
+          T u[VEC];
+          VecIO<T, VEC>::ldg(U + (size_t)j * a.np + off, u);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[j] += u[e] * xh[e];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) cta_stage((double)acc[j], sm, j, K + 1);
+  cta_stage(bad ? 1.0 : 0.0, sm, K, K + 1);
+  if (!cta_finish(a, s, sm, K + 1, red)) return;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (red[K] > 0.0) {
+      if (lane == 0) {
+        c->status = ST_NONFINITE;
+        c->t = step_size(a, c->frame_index);
+        write_info(c, a, s);
+      }
+    } else if (lane < a.k) {
+      c->y[lane] = red[lane];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_pass0: r = x - U y, its cost and coordinate gradient (fit.py:96-104).
+
+template <typename T, int K, int VEC>
+__global__ void __launch_bounds__(NT) k_pass0(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go, upd;
+  __shared__ double sstd, sseen, sy[K];
+  if (threadIdx.x == 0) {
+    go = c->status == ST_OK;
+    upd = c->update_stats;
+    sstd = c->std_cur;
+    sseen = (double)c->pseen;
+  }
+  if (threadIdx.x < K) sy[threadIdx.x] = threadIdx.x < a.k ? c->y[threadIdx.x] : 0.0;
+  __syncthreads();
+  if (!go) return;
+  constexpr int NV = K + 3;
+  __shared__ double sm[NW * NV];
+  __shared__ double red[NV];
+  T y[K], acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    y[j] = (T)sy[j];
+    acc[j] = (T)0;
+  }
+  double cost = 0.0;
+  T gsq = (T)0;
+  bool bad = false;
+  const int ng = a.Pp / VEC;
+  const T* U = static_cast<const T*>(a.U) + (size_t)s * a.k * a.np;
+  T* R = static_cast<T*>(a.r) + (size_t)s * a.np;
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    T w[VEC];
+    load_weights<T, VEC>(a, L, pix, w);
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T xh[VEC];
+      normalized<T, VEC>(a, (size_t)s * a.np + off, upd, true, (T)sseen, (T)sstd, xh, bad);
+      T u[K][VEC];
+      T uy[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) uy[e] = (T)0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < a.k) {
+          VecIO<T, VEC>::ldg(U + (size_t)j * a.np + off, u[j]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) u[j][e] = (T)0;
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) uy[e] += u[j][e] * y[j];
+      }
+      T r[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        r[e] = sub_rn(xh[e], uy[e]);
+        T tw, g;
+        penalty(r[e], w[e], a, tw, g);
+        cost += (double)tw;
+        gsq += g * g;
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] += u[j][e] * g;
+      }
+      VecIO<T, VEC>::st(R + off, r);
+    }
+  }
+  cta_stage(cost, sm, 0, NV);
+#pragma unroll
+  for (int j = 0; j < K; ++j) cta_stage((double)acc[j], sm, 1 + j, NV);
+  cta_stage((double)gsq, sm, K + 1, NV);
+  cta_stage(bad ? 1.0 : 0.0, sm, K + 2, NV);
+  if (!cta_finish(a, s, sm, NV, red)) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  if (red[K + 2] > 0.0) {
+    if (lane == 0) {
+      c->status = ST_NONFINITE;
+      c->t = step_size(a, c->frame_index);
+      write_info(c, a, s);
+    }
+    return;
+  }
+  if (lane < a.k) {
+    const double gj = -red[1 + lane];  // fit.py:101: grad = -(U^T g)
+    c->grad[lane] = gj;
+    c->d[lane] = -gj;
+  }
+  if (lane == 0) {
+    c->f = red[0];
+    c->gsq = red[K + 1];
+    c->it = 0;
+    c->iterations = 0;
+    c->cost_evals = 1;
+    c->grad_evals = 1;
+    c->pend_alpha = 0.0;
+  }
+  __syncwarp();
+  begin_iteration(c, a, s, lane);
+}
+
+// ---------------------------------------------------------------------------
+// k_iter: one CG iteration's U pass (fit.py:108-141).
+
+template <typename T, int K, int VEC>
+__global__ void __launch_bounds__(NT) k_iter(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go, lo;
+  __shared__ double sd[K], spend;
+  if (threadIdx.x == 0) {
+    go = c->status == ST_OK && c->active;
+    lo = c->gwin_lo;
+    spend = c->pend_alpha;
+  }
+  if (threadIdx.x < K) sd[threadIdx.x] = threadIdx.x < a.k ? c->d[threadIdx.x] : 0.0;
+  __syncthreads();
+  if (!go) return;
+  constexpr int NV = WC + WG * (K + 1);
+  __shared__ double sm[NW * NV];
+  __shared__ double red[NV];
+  T d[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) d[j] = (T)sd[j];
+  T al[WC];
+  {
+    double v = a.step0;
+#pragma unroll
+    for (int m = 0; m < WC; ++m) {
+      al[m] = (T)v;
+      v *= a.shrink;
+    }
+  }
+  const T pend = (T)spend;
+  const int wlo = lo;
+  double cost[WC];
+#pragma unroll
+  for (int m = 0; m < WC; ++m) cost[m] = 0.0;
+  T gacc[WG][K], gsq[WG];
+#pragma unroll
+  for (int mm = 0; mm < WG; ++mm) {
+    gsq[mm] = (T)0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) gacc[mm][j] = (T)0;
+  }
+  const int ng = a.Pp / VEC;
+  const T* U = static_cast<const T*>(a.U) + (size_t)s * a.k * a.np;
+  T* R = static_cast<T*>(a.r) + (size_t)s * a.np;
+  T* UD = static_cast<T*>(a.ud) + (size_t)s * a.np;
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    T w[VEC];
+    load_weights<T, VEC>(a, L, pix, w);
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T r[VEC], ud[VEC];
+      VecIO<T, VEC>::ld(R + off, r);
+      if (spend != 0.0) {
+        VecIO<T, VEC>::ld(UD + off, ud);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) r[e] = trial(r[e], pend, ud[e]);
+        VecIO<T, VEC>::st(R + off, r);
+      }
+      T u[K][VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) ud[e] = (T)0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < a.k) {
+          VecIO<T, VEC>::ldg(U + (size_t)j * a.np + off, u[j]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) u[j][e] = (T)0;
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) ud[e] += u[j][e] * d[j];
+      }
+      VecIO<T, VEC>::st(UD + off, ud);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        T gs[WG];
+#pragma unroll
+        for (int mm = 0; mm < WG; ++mm) gs[mm] = (T)0;
+#pragma unroll
+        for (int m = 0; m < WC; ++m) {
+          T tw, g;
+          penalty(trial(r[e], al[m], ud[e]), w[e], a, tw, g);
+          cost[m] += (double)tw;
+#pragma unroll
+          for (int mm = 0; mm < WG; ++mm)
+            if (m == wlo + mm) gs[mm] = g;
+        }
+#pragma unroll
+        for (int mm = 0; mm < WG; ++mm) {
+          gsq[mm] += gs[mm] * gs[mm];
+#pragma unroll
+          for (int j = 0; j < K; ++j) gacc[mm][j] += u[j][e] * gs[mm];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < WC; ++m) cta_stage(cost[m], sm, m, NV);
+#pragma unroll
+  for (int mm = 0; mm < WG; ++mm) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) cta_stage((double)gacc[mm][j], sm, WC + mm * (K + 1) + j, NV);
+    cta_stage((double)gsq[mm], sm, WC + mm * (K + 1) + K, NV);
+  }
+  if (!cta_finish(a, s, sm, NV, red)) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  // First acceptable step in the window (fit.py:126-135), sequential semantics.
+  const int nmax = a.max_bt < WC ? a.max_bt : WC;
+  int first = -1;
+  double alpha = a.step0;
+  for (int m = 0; m < nmax; ++m) {
+    if (red[m] <= c->f + a.c_armijo * alpha * c->slope) {
+      first = m;
+      break;
+    }
+    alpha *= a.shrink;
+  }
+  if (lane == 0) c->pend_alpha = 0.0;  // applied by this kernel
+  __syncwarp();
+  if (first >= 0) {
+    const int mm = first - wlo;
+    if (lane == 0) {
+      c->cost_evals += first + 1;
+      c->last_acc = first;
+    }
+    __syncwarp();
+    if (mm >= 0 && mm < WG) {
+      complete_iteration(c, a, s, lane, alpha, red[first], red + WC + mm * (K + 1),
+                         red[WC + mm * (K + 1) + K]);
+    } else if (lane == 0) {
+      c->need_gradfb = 1;
+      c->acc_idx = first;
+      c->acc_alpha = alpha;
+      c->acc_cost = red[first];
+    }
+  } else {
+    if (lane == 0) c->cost_evals += nmax;
+    __syncwarp();
+    if (nmax >= a.max_bt) {
+      fail_iteration(c, a, s, lane);
+    } else if (lane == 0) {
+      c->need_lsfb = 1;
+      c->ls_next = nmax;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_lsfb: further Armijo trials over the stored residual and u_dir only.
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(NT) k_lsfb(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go, m0;
+  if (threadIdx.x == 0) {
+    go = c->status == ST_OK && c->active && c->need_lsfb;
+    m0 = c->ls_next;
+  }
+  __syncthreads();
+  if (!go) return;
+  __shared__ double sm[NW * LSW];
+  __shared__ double red[LSW];
+  const int base = m0;
+  const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
+  T al[LSW];
+  {
+    double v = alpha_at(a, base);
+#pragma unroll
+    for (int m = 0; m < LSW; ++m) {
+      al[m] = (T)v;
+      v *= a.shrink;
+    }
+  }
+  double cost[LSW];
+#pragma unroll
+  for (int m = 0; m < LSW; ++m) cost[m] = 0.0;
+  const int ng = a.Pp / VEC;
+  const T* R = static_cast<const T*>(a.r) + (size_t)s * a.np;
+  const T* UD = static_cast<const T*>(a.ud) + (size_t)s * a.np;
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    T w[VEC];
+    load_weights<T, VEC>(a, L, pix, w);
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T r[VEC], ud[VEC];
+      VecIO<T, VEC>::ld(R + off, r);
+      VecIO<T, VEC>::ld(UD + off, ud);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+#pragma unroll
+        for (int m = 0; m < LSW; ++m) {
+          if (m < cnt) {
+            T tw, g;
+            penalty(trial(r[e], al[m], ud[e]), w[e], a, tw, g);
+            cost[m] += (double)tw;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < LSW; ++m) cta_stage(cost[m], sm, m, LSW);
+  if (!cta_finish(a, s, sm, LSW, red)) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  int first = -1;
+  double alpha = alpha_at(a, base);
+  for (int m = 0; m < cnt; ++m) {
+    if (red[m] <= c->f + a.c_armijo * alpha * c->slope) {
+      first = m;
+      break;
+    }
+    alpha *= a.shrink;
+  }
+  if (first >= 0) {
+    if (lane == 0) {
+      c->cost_evals += first + 1;
+      c->need_lsfb = 0;
+      c->need_gradfb = 1;
+      c->last_acc = base + first;
+      c->acc_idx = base + first;
+      c->acc_alpha = alpha;
+      c->acc_cost = red[first];
+    }
+  } else {
+    if (lane == 0) c->cost_evals += cnt;
+    __syncwarp();
+    if (base + cnt >= a.max_bt) {
+      if (lane == 0) c->need_lsfb = 0;
+      __syncwarp();
+      fail_iteration(c, a, s, lane);
+    } else if (lane == 0) {
+      c->ls_next = base + cnt;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_gradfb: coordinate gradient at an accepted step outside the window.
+
+template <typename T, int K, int VEC>
+__global__ void __launch_bounds__(NT) k_gradfb(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go;
+  __shared__ double salpha;
+  if (threadIdx.x == 0) {
+    go = c->status == ST_OK && c->active && c->need_gradfb;
+    salpha = c->acc_alpha;
+  }
+  __syncthreads();
+  if (!go) return;
+  constexpr int NV = K + 1;
+  __shared__ double sm[NW * NV];
+  __shared__ double red[NV];
+  const T alpha = (T)salpha;
+  T acc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) acc[j] = (T)0;
+  T gsq = (T)0;
+  const int ng = a.Pp / VEC;
+  const T* U = static_cast<const T*>(a.U) + (size_t)s * a.k * a.np;
+  const T* R = static_cast<const T*>(a.r) + (size_t)s * a.np;
+  const T* UD = static_cast<const T*>(a.ud) + (size_t)s * a.np;
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    T w[VEC];
+    load_weights<T, VEC>(a, L, pix, w);
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T r[VEC], ud[VEC], g[VEC];
+      VecIO<T, VEC>::ld(R + off, r);
+      VecIO<T, VEC>::ld(UD + off, ud);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        T tw;
+        penalty(trial(r[e], alpha, ud[e]), w[e], a, tw, g[e]);
+        gsq += g[e] * g[e];
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < a.k) {
+          T u[VEC];
+          VecIO<T, VEC>::ldg(U + (size_t)j * a.np + off, u);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[j] += u[e] * g[e];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) cta_stage((double)acc[j], sm, j, NV);
+  cta_stage((double)gsq, sm, K, NV);
+  if (!cta_finish(a, s, sm, NV, red)) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  if (lane == 0) c->need_gradfb = 0;
+  __syncwarp();
+  complete_iteration(c, a, s, lane, c->acc_alpha, c->acc_cost, red, red[K]);
+}
+
+// ---------------------------------------------------------------------------
+// k_geo: rank-one geodesic step of U along the projected gradient, then the
+// relabel / background / residual epilogue against the updated basis.
+// QR = true: apply the inverse Cholesky factor of U'^T U' instead (periodic
+// re-orthonormalization, manifold.py:192-196) and run the same epilogue.
+
+template <typename T, int K, int VEC, bool QR>
+__global__ void __launch_bounds__(NT) k_geo(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go, dogeo, relabel;
+  __shared__ double sv[K], sg[K], sy[K], sc[6];
+  __shared__ double srinv[QR ? K * K : 1];
+  if (threadIdx.x == 0) {
+    go = c->status == ST_OK && (!QR || c->qr_now);
+    dogeo = QR ? 1 : c->do_geo;
+    relabel = QR ? 1 : !c->qr_now;
+    sc[0] = c->geo_a;
+    sc[1] = c->geo_s;
+    sc[2] = c->geo_ln;
+    sc[3] = c->pend_alpha;
+    sc[4] = c->std_cur;
+  }
+  if (threadIdx.x < K) {
+    const int j = threadIdx.x;
+    sv[j] = j < a.k ? c->v[j] : 0.0;
+    sg[j] = j < a.k ? c->grad[j] : 0.0;
+    sy[j] = j < a.k ? c->y[j] : 0.0;
+  }
+  if (QR) {
+    for (int i = threadIdx.x; i < K * K; i += NT) {
+      const int l = i / K, j = i % K;
+      srinv[i] = (l < a.k && j < a.k) ? a.rinv[(size_t)s * KMAX * KMAX + l * KMAX + j] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!go) return;
+  const T ga = (T)sc[0], gsn = (T)sc[1], ln = (T)sc[2], pend = (T)sc[3], stdv = (T)sc[4];
+  const bool do_geo = dogeo, do_lab = relabel;
+  T v[K], gr[K], y[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    v[j] = (T)sv[j];
+    gr[j] = (T)sg[j];
+    y[j] = (T)sy[j];
+  }
+  const int ng = a.Pp / VEC;
+  T* U = static_cast<T*>(a.U) + (size_t)s * a.k * a.np;
+  const T* R = static_cast<const T*>(a.r) + (size_t)s * a.np;
+  const T* UD = static_cast<const T*>(a.ud) + (size_t)s * a.np;
+  uint8_t* L = a.lab + (size_t)s * a.Pp;
+  T* BG = a.bg_out ? static_cast<T*>(a.bg_out) + (size_t)s * a.np : nullptr;
+  T* RES = a.res_out ? static_cast<T*>(a.res_out) + (size_t)s * a.np : nullptr;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    T w[VEC];
+    load_weights<T, VEC>(a, L, pix, w);
+    T mx[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) mx[e] = (T)0;
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T u[K][VEC];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < a.k) {
+          VecIO<T, VEC>::ld(U + (size_t)j * a.np + off, u[j]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) u[j][e] = (T)0;
+        }
+      }
+      if (do_geo) {
+        if constexpr (QR) {
+          // U'' = U' R^{-1} (R upper triangular)
+          T nu[K][VEC];
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) nu[j][e] = (T)0;
+#pragma unroll
+            for (int l = 0; l <= j; ++l) {
+              const T rl = (T)srinv[l * K + j];
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) nu[j][e] += u[l][e] * rl;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) u[j][e] = nu[j][e];
+        } else {
+          T r[VEC], ud[VEC];
+          VecIO<T, VEC>::ld(R + off, r);
+          if (sc[3] != 0.0) {
+            VecIO<T, VEC>::ld(UD + off, ud);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) r[e] = trial(r[e], pend, ud[e]);
+          }
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            T tw, g;
+            penalty(r[e], w[e], a, tw, g);
+            const T eta = -g;  // cost.py:103-112
+            T uv = (T)0, ug = (T)0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              uv += u[j][e] * v[j];
+              ug += u[j][e] * gr[j];
+            }
+            const T proj = eta - ug;  // manifold.py:127
+            const T coef = ga * uv - gsn * (proj / ln);
+#pragma unroll
+            for (int j = 0; j < K; ++j) u[j][e] += coef * v[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          if (j < a.k) VecIO<T, VEC>::st(U + (size_t)j * a.np + off, u[j]);
+      }
+      if (do_lab) {
+        T xh[VEC];
+        bool bad = false;
+        normalized<T, VEC>(a, (size_t)s * a.np + off, false, false, (T)1, stdv, xh, bad);
+        T bgn[VEC], rr[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          T acc = (T)0;
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc += u[j][e] * y[j];
+          bgn[e] = acc;
+          rr[e] = sub_rn(xh[e], acc);
+          mx[e] = fmax(mx[e], fabs(rr[e]));
+        }
+        if (RES) VecIO<T, VEC>::st(RES + off, rr);
+        if (BG) {
+          T b[VEC];
+          if (a.pipeline) {
+            T mv[VEC];
+            VecIO<T, VEC>::ld(static_cast<const T*>(a.mean) + (size_t)s * a.np + off, mv);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+              b[e] = fmin(fmax(add_rn(bgn[e] * stdv, mv[e]), (T)0), (T)1);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) b[e] = bgn[e];
+          }
+          VecIO<T, VEC>::st(BG + off, b);
+        }
+      }
+    }
+    if (do_lab) {
+      uint8_t lb[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        lb[e] = (pix + e < a.P && (double)mx[e] >= a.delta) ? 1 : 0;
+      st_lab<VEC>(L + pix, lb);
+      if (a.raw_out) st_lab<VEC>(a.raw_out + (size_t)s * a.Pp + pix, lb);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_gram: G = U'^T U' for streams due for re-orthonormalization; the last CTA
+// factors G = R^T R (Cholesky, R upper with positive diagonal — the same Q as
+// the reference's sign-fixed Householder QR) and stores R^{-1}.
+
+template <typename T, int K, int VEC>
+__global__ void __launch_bounds__(NT) k_gram(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  Ctl* c = a.ctl + s;
+  __shared__ int go;
+  if (threadIdx.x == 0) go = c->status == ST_OK && c->qr_now;
+  __syncthreads();
+  if (!go) return;
+  constexpr int NP = K * (K + 1) / 2;
+  __shared__ double sm[NW * NP];
+  __shared__ double red[NP];
+  const int k = a.k;
+  const int np_ = k * (k + 1) / 2;
+  const int ng = a.Pp / VEC;
+  const T* U = static_cast<const T*>(a.U) + (size_t)s * a.k * a.np;
+  int pr = 0;
+  for (int ia = 0; ia < k; ++ia) {
+    for (int ib = ia; ib < k; ++ib, ++pr) {
+      double acc = 0.0;
+      for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+        const int pix = q * VEC;
+        for (int ch = 0; ch < a.C; ++ch) {
+          const size_t off = (size_t)ch * a.Pp + pix;
+          T ua[VEC], ub[VEC];
+          VecIO<T, VEC>::ld(U + (size_t)ia * a.np + off, ua);
+          VecIO<T, VEC>::ld(U + (size_t)ib * a.np + off, ub);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc += (double)ua[e] * (double)ub[e];
+        }
+      }
+      cta_stage(acc, sm, pr, np_);
+    }
+  }
+  if (!cta_finish(a, s, sm, np_, red)) return;
+  if (threadIdx.x != 0) return;
+  // G (packed upper triangle) is in red; R lives in shared memory.
+  __shared__ double Rm[KMAX * KMAX];
+  auto Gat = [&](int i, int j) {
+    if (i > j) { const int t = i; i = j; j = t; }
+    return red[i * k - i * (i - 1) / 2 + (j - i)];
+  };
+  for (int i = 0; i < KMAX * KMAX; ++i) Rm[i] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    double dsum = Gat(j, j);
+    for (int l = 0; l < j; ++l) dsum -= Rm[l * KMAX + j] * Rm[l * KMAX + j];
+    const double rjj = sqrt(fmax(dsum, 1e-300));
+    Rm[j * KMAX + j] = rjj;
+    for (int i = j + 1; i < k; ++i) {
+      double o = Gat(j, i);
+      for (int l = 0; l < j; ++l) o -= Rm[l * KMAX + j] * Rm[l * KMAX + i];
+      Rm[j * KMAX + i] = o / rjj;
+    }
+  }
+  // R^{-1}, upper triangular, column by column
+  double* Ri = a.rinv + (size_t)s * KMAX * KMAX;
+  for (int i = 0; i < KMAX * KMAX; ++i) Ri[i] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    Ri[j * KMAX + j] = 1.0 / Rm[j * KMAX + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double o = 0.0;
+      for (int l = i + 1; l <= j; ++l) o += Rm[i * KMAX + l] * Ri[l * KMAX + j];
+      Ri[i * KMAX + j] = -o / Rm[i * KMAX + i];
+    }
+  }
+  c->since_qr = 0;
+}
+
+// ---------------------------------------------------------------------------
+// k_median: 3x3 majority vote with edge replication (pipeline.py:215-228).
+
+__global__ void __launch_bounds__(NT) k_median(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  if (a.ctl[s].status != ST_OK) return;
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  uint8_t* M = a.mask_out + (size_t)s * a.Pp;
+  const int W = a.width, H = a.height;
+  for (int p = blockIdx.x * NT + threadIdx.x; p < a.P; p += gridDim.x * NT) {
+    const int yy = p / W, xx = p - yy * W;
+    int votes = 0;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int ry = min(max(yy + dy, 0), H - 1);
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int rx = min(max(xx + dx, 0), W - 1);
+        votes += L[ry * W + rx];
+      }
+    }
+    M[p] = votes >= 5 ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_background: clip((U y) * scale + mean, 0, 1) (jobs.py:231-239).
+
+template <typename T, int K, int VEC>
+__global__ void __launch_bounds__(NT) k_background(Args a) {
+  const int s = a.s0 + blockIdx.y;
+  const Ctl* c = a.ctl + s;
+  __shared__ double sy[K], sscale;
+  if (threadIdx.x < K) sy[threadIdx.x] = threadIdx.x < a.k ? c->y[threadIdx.x] : 0.0;
+  if (threadIdx.x == 0) sscale = c->frozen ? c->pstd : running_std(c);
+  __syncthreads();
+  const T scale = (T)sscale;
+  const T* U = static_cast<const T*>(a.U) + (size_t)s * a.k * a.np;
+  const T* M = static_cast<const T*>(a.mean) + (size_t)s * a.np;
+  T* BG = static_cast<T*>(a.bg_out) + (size_t)s * a.np;
+  const int ng = a.Pp / VEC;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
+    const int pix = q * VEC;
+    for (int ch = 0; ch < a.C; ++ch) {
+      const size_t off = (size_t)ch * a.Pp + pix;
+      T acc[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = (T)0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        if (j < a.k) {
+          T u[VEC];
+          VecIO<T, VEC>::ld(U + (size_t)j * a.np + off, u);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] += u[e] * (T)sy[j];
+        }
+      }
+      T mv[VEC], b[VEC];
+      VecIO<T, VEC>::ld(M + off, mv);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) b[e] = fmin(fmax(add_rn(acc[e] * scale, mv[e]), (T)0), (T)1);
+      VecIO<T, VEC>::st(BG + off, b);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// layout conversion between dense user arrays [S][C][P] and padded [S][C][Pp]
+
+template <typename TS, typename TD>
+__global__ void k_pack(const TS* __restrict__ src, TD* __restrict__ dst, int S, int C, int P,
+                       int Pp, int to_padded, double scale) {
+  const long long total = (long long)S * C * P;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / P;
+    const int p = (int)(i - row * P);
+    const long long dense = i, padded = row * Pp + p;
+    if (to_padded) dst[padded] = (TD)((double)src[dense] * scale);
+    else dst[dense] = (TD)((double)src[padded] * scale);
+  }
+}
+
+}  // namespace prost

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+vectors and the CPU oracle.
+
+Two instantiations are checked:
+  * fp64 (parity instantiation): one-step agreement with the reference to
+    1e-10 and identical decisions (CG iterations / Armijo evaluations / labels);
+  * fp32 (the product path): north_star tolerances — principal-angle sine of U
+    <= 1e-3, background relative L2 <= 1e-4, mask disagreement <= 0.1% — plus a
+    teacher-forced one-step bound of 1e-5 on the angle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import prost_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+pkg = pytest.importorskip("paper_1302_2073_b200")
+
+
+def load(name):
+    return np.load(GOLDEN / f"{name}.npz")
+
+
+def traj_params(z):
+    k, p, mu, delta, omega, t_init, t_min, tau, iters, seed = z["prm"]
+    params = pkg.ProstParams(k=int(k), cfg=pkg.LpConfig(p=p, mu=mu), delta=delta, omega=omega,
+                             t_init=t_init, t_min=t_min, tau=tau,
+                             cg=pkg.CgOptions(max_iters=int(iters)))
+    return params, int(seed)
+
+
+def sine(A, B):
+    return orc.subspace_sine(A, B)
+
+
+# ---------------------------------------------------------------------------
+# process_frame (tracker.py:121-156), teacher forced along the reference
+# trajectory: every frame starts from the reference's own state.
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_process_frame_teacher_forced(precision):
+    z = load("step_trajectory")
+    params, seed = traj_params(z)
+    frames = z["frames"]
+    U_prev = z["U0"]
+    y_prev = np.zeros(params.k)
+    w_prev = np.ones(frames.shape[1])
+    same_counts = 0
+    for i, x in enumerate(frames):
+        st = pkg.TrackerState(pkg.SubspaceBasis(U_prev), y_prev, w_prev, frame_index=i)
+        new, r, fit = pkg.process_frame(st, x, params, precision=precision)
+        assert new.frame_index == i + 1
+        same = [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z["counts"][i])
+        same_counts += same
+        if precision == "fp64":
+            assert same, (i, fit, z["counts"][i])
+            np.testing.assert_allclose(new.basis.data, z["U"][i], rtol=0, atol=1e-10)
+            np.testing.assert_allclose(new.y, z["y"][i], rtol=1e-10, atol=1e-10)
+            np.testing.assert_allclose(r, z["residual"][i], rtol=0, atol=1e-9)
+            np.testing.assert_array_equal(new.weights, z["w"][i])
+            assert fit.cost == pytest.approx(z["cost"][i], rel=1e-12)
+        else:
+            assert sine(new.basis.data, z["U"][i]) <= 1e-5
+            np.testing.assert_allclose(r, z["residual"][i], rtol=0, atol=1e-4)
+            assert np.mean(new.weights != z["w"][i]) <= 0.01
+            assert fit.cost == pytest.approx(z["cost"][i], rel=1e-5)
+        U_prev, y_prev, w_prev = z["U"][i], z["y"][i], z["w"][i]
+    assert same_counts >= 0.95 * len(frames)
+
+
+def test_process_frame_free_running_fp64():
+    z = load("step_trajectory")
+    params, seed = traj_params(z)
+    st = pkg.bootstrap(z["frames"].shape[1], params, seed)
+    np.testing.assert_array_equal(st.basis.data, z["U0"])
+    for i, x in enumerate(z["frames"]):
+        st, r, fit = pkg.process_frame(st, x, params, precision="fp64")
+        assert sine(st.basis.data, z["U"][i]) <= 1e-9
+        np.testing.assert_array_equal(st.weights, z["w"][i])
+        assert fit.cost == pytest.approx(z["cost"][i], rel=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_fit_cases(precision):
+    """fit_coordinates golden cases (p = 0.5, 0.25, 2, 1; cold and warm starts),
+    observed through process_frame's fitted coordinates and counters."""
+    z = load("fit_vectors")
+    for case in range(4):
+        key = f"c{case}_"
+        p, mu, iters = z[key + "prm"]
+        U = z[key + "U"]
+        m, k = U.shape
+        params = pkg.ProstParams(k=k, cfg=pkg.LpConfig(p=p, mu=mu), delta=0.35, omega=5e-5,
+                                 cg=pkg.CgOptions(max_iters=int(iters)))
+        y0 = z[key + "y0"]
+        cold = bool(np.isnan(y0).all())
+        st = pkg.TrackerState(pkg.SubspaceBasis(U), np.zeros(k) if cold else y0, z[key + "w"],
+                              frame_index=0 if cold else 1)
+        _, _, fit = pkg.process_frame(st, z[key + "x"], params, precision=precision)
+        tol = 1e-10 if precision == "fp64" else 2e-4
+        np.testing.assert_allclose(fit.y, z[key + "y"], rtol=tol, atol=tol)
+        assert fit.cost == pytest.approx(float(z[key + "cost"]), rel=tol)
+        if precision == "fp64":
+            assert [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z[key + "counts"])
+
+
+def test_periodic_reorthonormalization_fp64():
+    """The unconditional QR at the 1000th geodesic step (manifold.py:192-196),
+    replayed from the reference's state at step 997."""
+    z = load("qr_chain")
+    params = pkg.ProstParams(k=3, cfg=pkg.LpConfig(p=0.5, mu=0.06125), delta=0.35, omega=5e-5,
+                             t_init=1e-2, t_min=1e-3, tau=1e-3, cg=pkg.CgOptions(max_iters=2))
+    # rebuild the reference state at frame 997 with the oracle (pinned bit-exact)
+    oprm = orc.OracleParams(k=3, p=0.5, mu=0.06125, delta=0.35, omega=5e-5, t_init=1e-2,
+                            t_min=1e-3, tau=1e-3, max_iters=2)
+    ost = orc.core_init(48, oprm, 3)
+    for x in z["frames"][:998]:
+        ost, _, _ = orc.core_step(ost, x, oprm)
+    np.testing.assert_array_equal(ost.U, z["U997"])
+    st = pkg.TrackerState(pkg.SubspaceBasis(ost.U, steps_since_qr=ost.since_qr), ost.y, ost.w,
+                          frame_index=ost.frame_index)
+    for i in range(998, 1003):
+        st, _, _ = pkg.process_frame(st, z["frames"][i], params, precision="fp64")
+        np.testing.assert_allclose(st.basis.data, z[f"U{i}"], rtol=0, atol=1e-10)
+        assert st.basis.steps_since_qr == int(z[f"since{i}"])
+
+
+def test_rejects_non_finite_frame_without_mutation():
+    z = load("step_trajectory")
+    params, seed = traj_params(z)
+    st = pkg.bootstrap(z["frames"].shape[1], params, seed)
+    st, _, _ = pkg.process_frame(st, z["frames"][0], params)
+    bad = z["frames"][1].copy()
+    bad[7] = np.nan
+    with pytest.raises(pkg.NonFiniteError):
+        pkg.process_frame(st, bad, params)
+    with pytest.raises(pkg.DimensionError):
+        pkg.process_frame(st, bad[:-1], params)
+    # the functional seam never mutates its input; the next good frame proceeds
+    st2, _, _ = pkg.process_frame(st, z["frames"][1], params, precision="fp64")
+    assert st2.frame_index == 2
+
+
+# ---------------------------------------------------------------------------
+# StreamTracker.push (jobs.py:186-239) against the reference's own run
+
+
+@pytest.mark.parametrize("name", ["push_gray", "push_rgb"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_stream_tracker_golden(name, precision):
+    z = load(name)
+    k, p, mu, iters, i_init, seed, channels = z["cfg"]
+    cfg = pkg.RunConfig(subspace_dim=int(k), p=p, mu=mu, cg_max_iters=int(iters), target_width=32,
+                        target_height=24, grayscale=False, i_init=int(i_init), seed=int(seed))
+    tr = pkg.StreamTracker(cfg, precision=precision)
+    for i, v in enumerate(z["frames"]):
+        rec = tr.push(pkg.FrameBuffer(32, 24, int(channels), v))
+        assert rec.frame_index == i + 1
+        assert rec.step == z["step"][i]
+        bg = tr.background_frame().data
+        if precision == "fp64":
+            np.testing.assert_array_equal(rec.raw_mask.labels, z["raw_mask"][i])
+            np.testing.assert_array_equal(rec.mask.labels, z["mask"][i])
+            np.testing.assert_allclose(rec.residual, z["residual"][i], rtol=0, atol=1e-9)
+            assert rec.fit_cost == pytest.approx(z["fit_cost"][i], rel=1e-10)
+            np.testing.assert_allclose(bg, z["background"][i], rtol=0, atol=1e-10)
+        else:
+            assert np.mean(rec.raw_mask.labels != z["raw_mask"][i]) <= 0.001
+            assert np.mean(rec.mask.labels != z["mask"][i]) <= 0.001
+            ref_bg = z["background"][i]
+            assert np.linalg.norm(bg - ref_bg) <= 1e-4 * np.linalg.norm(ref_bg)
+            assert rec.fit_cost == pytest.approx(z["fit_cost"][i], rel=1e-4)
+    st = tr.state
+    tol = 1e-9 if precision == "fp64" else 1e-3
+    assert sine(st.basis.data, z["U"]) <= tol
+    np.testing.assert_allclose(tr.stats.mean, z["mean"], rtol=0, atol=1e-12 if precision == "fp64" else 1e-6)
+    assert tr.stats.std == pytest.approx(float(z["std"]), rel=1e-12)
+
+
+def test_stream_tracker_rejects_bad_input():
+    cfg = pkg.RunConfig(subspace_dim=4, target_width=16, target_height=8, grayscale=False, i_init=3)
+    tr = pkg.StreamTracker(cfg)
+    rng = np.random.default_rng(0)
+    tr.push(pkg.FrameBuffer(16, 8, 1, rng.random(128)))
+    with pytest.raises(pkg.SequenceError):  # jobs.py:195-198
+        tr.push(pkg.FrameBuffer(16, 8, 3, rng.random(384)))
+    with pytest.raises(pkg.DimensionError):
+        tr.push(pkg.FrameBuffer(8, 8, 1, rng.random(64)))
+    bad = rng.random(128)
+    bad[3] = np.inf
+    with pytest.raises(pkg.NonFiniteError):
+        tr.push(pkg.FrameBuffer(16, 8, 1, bad))
+    assert tr.frame_index == 1
+    rec = tr.push(pkg.FrameBuffer(16, 8, 1, rng.random(128)))
+    assert rec.frame_index == 2
+
+
+# ---------------------------------------------------------------------------
+# larger configurations: oracle comparison at the C0 shape and batched streams
+
+
+def c0_stream(n_frames, width=160, height=120, seed=0):
+    from paper_1302_2073_b200.synth import SceneSpec, SceneStream
+
+    spec = SceneSpec(width=width, height=height, channels=1, rank=5, noise=0.02, seed=seed)
+    return SceneStream(spec).next_frames(n_frames)
+
+
+def oracle_for(cfg, i_init, width, height, channels=1):
+    prm = cfg.params(i_init)
+    return orc.PipelineOracle(width, height, channels, orc.OracleParams(
+        k=prm.k, p=prm.cfg.p, mu=prm.cfg.mu, delta=prm.delta, omega=prm.omega,
+        t_init=prm.t_init, t_min=prm.t_min, tau=prm.tau, max_iters=prm.cg.max_iters),
+        i_init=i_init, seed=cfg.seed)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_c0_shape_against_oracle(precision):
+    """C0 shape (160x120, k=15, p=0.5, mu=1e-4, 2 CG iterations), 60 frames
+    through the init window: masks, background and basis against the oracle."""
+    n_frames, i_init = 60, 20
+    frames = c0_stream(n_frames)
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=160,
+                        target_height=120, grayscale=True, i_init=i_init, seed=0)
+    tr = pkg.StreamTracker(cfg, precision=precision)
+    ref = oracle_for(cfg, i_init, 160, 120)
+    worst = 0.0
+    for v in frames:
+        a = tr.push(pkg.FrameBuffer(160, 120, 1, v))
+        b = ref.push(v)
+        worst = max(worst, float(np.mean(a.mask.labels != b.mask)))
+        if precision == "fp64":
+            np.testing.assert_array_equal(a.raw_mask.labels, b.raw_mask)
+            assert a.fit_cost == pytest.approx(b.fit_cost, rel=1e-10)
+    bg = tr.background_frame().data
+    rbg = ref.background()
+    rel = np.linalg.norm(bg - rbg) / np.linalg.norm(rbg)
+    ang = sine(tr.state.basis.data, ref.state.U)
+    if precision == "fp64":
+        assert rel <= 1e-10 and ang <= 1e-9
+    else:
+        assert worst <= 0.001 and rel <= 1e-4 and ang <= 1e-3
+
+
+def test_batched_streams_bitwise_match_single_streams():
+    """Streams batched into one launch give bit-identical results to the same
+    streams run alone (deterministic fixed-order reductions)."""
+    import torch
+
+    W, H, S, F = 64, 48, 3, 8
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=4, seed=0)
+    streams = [c0_stream(F, W, H, seed=s) for s in range(S)]
+    bt = pkg.BatchTracker(cfg, S, seeds=[0, 1, 2])
+    masks = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+    out_b = []
+    for f in range(F):
+        frames = torch.from_numpy(np.stack([s[f] for s in streams]).astype(np.float32)).cuda()
+        bt.push(frames, mask=masks)
+        out_b.append(masks.cpu().numpy().copy())
+    bt.synchronize()
+    for s in range(S):
+        single = pkg.BatchTracker(cfg, 1, seeds=[s])
+        m1 = torch.empty((1, W * H), dtype=torch.uint8, device="cuda")
+        for f in range(F):
+            single.push(torch.from_numpy(streams[s][f][None].astype(np.float32)).cuda(), mask=m1)
+            np.testing.assert_array_equal(m1.cpu().numpy()[0], out_b[f][s])
+        Ub = bt.native.get_core_state(s)[0]
+        U1 = single.native.get_core_state(0)[0]
+        np.testing.assert_array_equal(Ub, U1)
+
+
+def test_large_batch_properties():
+    """C3 shape (320x240, k=15) with 8 streams for 6 frames: size-independent
+    properties — orthonormality, raw mask == threshold of the residual, mask ==
+    3x3 majority of the raw mask, background inside [0, 1]."""
+    import torch
+
+    W, H, S, F = 320, 240, 8, 6
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=3, seed=0)
+    bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    data = [c0_stream(F, W, H, seed=s) for s in range(S)]
+    n = W * H
+    mask = torch.empty((S, n), dtype=torch.uint8, device="cuda")
+    raw = torch.empty((S, n), dtype=torch.uint8, device="cuda")
+    res = torch.empty((S, n), dtype=torch.float32, device="cuda")
+    bg = torch.empty((S, n), dtype=torch.float32, device="cuda")
+    for f in range(F):
+        fr = torch.from_numpy(np.stack([d[f] for d in data]).astype(np.float32)).cuda()
+        info = bt.push(fr, background=bg, residual=res, mask=mask, raw_mask=raw, fit=True)
+        assert all(info[s].frame_index == f + 1 for s in range(S))
+        r = res.cpu().numpy()
+        rm = raw.cpu().numpy()
+        mk = mask.cpu().numpy()
+        np.testing.assert_array_equal(rm, (np.abs(r) >= 0.35).astype(np.uint8))
+        for s in range(S):
+            np.testing.assert_array_equal(mk[s], orc.majority3x3(rm[s], W, H))
+        b = bg.cpu().numpy()
+        assert b.min() >= 0.0 and b.max() <= 1.0
+    for s in range(S):
+        U = bt.native.get_core_state(s)[0]
+        assert np.linalg.norm(U.T @ U - np.eye(15)) < 1e-4
