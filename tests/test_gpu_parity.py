@@ -180,7 +180,7 @@ def test_stream_tracker_golden(name, precision):
     tol = 1e-9 if precision == "fp64" else 1e-3
     assert sine(st.basis.data, z["U"]) <= tol
     np.testing.assert_allclose(tr.stats.mean, z["mean"], rtol=0, atol=1e-12 if precision == "fp64" else 1e-6)
-    assert tr.stats.std == pytest.approx(float(z["std"]), rel=1e-12)
+    assert tr.stats.std == pytest.approx(float(z["std"]), rel=1e-12 if precision == "fp64" else 1e-6)
 
 
 def test_stream_tracker_rejects_bad_input():
