@@ -275,6 +275,13 @@ def main():
     bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev)
     if args.wave:
         bt.native.set_wave(args.wave)
+    from paper_1302_2073_b200 import _native as nat
+
+    if bt.native.query(nat.Q_RESIDENT):
+        kernel_path = (f"resident: {bt.native.query(nat.Q_TEAMS)} teams x "
+                       f"{bt.native.query(nat.Q_TEAM)} CTAs, one cooperative launch per step")
+    else:
+        kernel_path = f"streamed: {bt.native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel"
     mask = torch.empty((S, P), dtype=torch.uint8, device=f"cuda:{dev}")
     bg = torch.empty((S, n), dtype=torch.float32 if args.precision == "fp32" else torch.float64,
                      device=f"cuda:{dev}")
@@ -342,6 +349,7 @@ def main():
         step += 1
     torch.cuda.synchronize()
     phases = bt.native.profile_read()
+    resident_counters = bt.native.resident_counters() if bt.native.query(nat.Q_RESIDENT) else None
     bt.native.profile(False)
 
     # end to end through the public API: pinned host frames in, host mask + bg out
@@ -420,7 +428,8 @@ def main():
                                    f"p={cfg.p}, mu={cfg.mu}, cg_max_iters={cfg.cg_max_iters}",
                        "streams_per_gpu": S, "n": n, "k": k, "precision": args.precision,
                        "l2": "inputs larger than L2 (U alone is %.2f GB per GPU)" % (S * 4 * n * k / 1e9),
-                       "parallelism": f"stream-sharded x{ws}"},
+                       "parallelism": f"stream-sharded x{ws}",
+                       "kernel_path": kernel_path},
             "mpix_per_s": value * P / 1e6,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "frame update (all phase kernels of one step)",
@@ -429,6 +438,7 @@ def main():
                          "bytes_per_stream_frame": ba, "b_u_frac": (S * bu / (ms_step / 1e3) / 1e9) / peak,
                          "dominant_phase": dom},
             "phases": phase_out,
+            "resident_counters": resident_counters,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

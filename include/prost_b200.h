@@ -148,6 +148,9 @@ int prost_last_error(prost_handle* h, char* buf, int32_t len);
 #define PROST_Q_BYTES_U 2
 #define PROST_Q_CHUNKS 3
 #define PROST_Q_INSTANCE_K 4
+#define PROST_Q_RESIDENT 5   /* 1 when frames run in the register-resident kernel */
+#define PROST_Q_TEAM 6       /* CTAs per team (resident mode) */
+#define PROST_Q_TEAMS 7      /* teams (resident mode) */
 int prost_query(prost_handle* h, int32_t what, int64_t* value);
 
 /* Per-phase device timing (CUDA events around every launch, on the launch
@@ -162,8 +165,14 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value);
 #define PROST_PH_GEO 6
 #define PROST_PH_QR 7
 #define PROST_PH_MEDIAN 8
-#define PROST_N_PHASES 9
+#define PROST_PH_FRAME 9   /* the register-resident whole-frame kernel */
+#define PROST_N_PHASES 10
 int prost_profile(prost_handle* h, int32_t enable);
+/* Resident-kernel timing of the last launch made with profiling on, as
+ * per-CTA means (%globaltimer ns): [0] kernel, [1] team-barrier waits,
+ * [2] slot reads, [3] scalar logic, [4] prefetch waits, [5] team reductions,
+ * [6] rounds, [7] unused, [8] (if n > 8) the slowest CTA's kernel time. */
+int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n);
 int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n_phases);
 
 /* Tuning knob: streams per launch wave (0 = automatic, sized to L2). */

@@ -20,14 +20,15 @@ ERR_CONFIG, ERR_DIMENSION, ERR_NONFINITE, ERR_SEQUENCE, ERR_CUDA = 1, 2, 3, 4, 5
 F32, F64, U8 = 0, 1, 2
 FLAG_PIPELINE, FLAG_FP64 = 1, 2
 Q_LAUNCHES, Q_WAVE, Q_BYTES_U, Q_CHUNKS, Q_INSTANCE_K = 0, 1, 2, 3, 4
+Q_RESIDENT, Q_TEAM, Q_TEAMS = 5, 6, 7
 
 EXPORTS = (
     "prost_abi_version", "prost_create", "prost_destroy", "prost_set_core_state",
     "prost_get_core_state", "prost_set_preproc", "prost_get_preproc", "prost_push",
     "prost_background", "prost_synchronize", "prost_last_error", "prost_query",
-    "prost_set_wave", "prost_profile", "prost_profile_read",
+    "prost_set_wave", "prost_profile", "prost_profile_read", "prost_resident_counters",
 )
-PHASES = ("stats", "cold", "pass0", "iter", "lsfb", "gradfb", "geo", "qr", "median")
+PHASES = ("stats", "cold", "pass0", "iter", "lsfb", "gradfb", "geo", "qr", "median", "frame")
 
 _ERRORS = {
     ERR_CONFIG: ConfigError,
@@ -101,6 +102,7 @@ def lib() -> ctypes.CDLL:
     L.prost_set_wave.argtypes = [vp, i32]
     L.prost_profile.argtypes = [vp, i32]
     L.prost_profile_read.argtypes = [vp, dp, ctypes.POINTER(i64), i32]
+    L.prost_resident_counters.argtypes = [vp, ctypes.POINTER(i64), i32]
     for name in EXPORTS:
         if name not in ("prost_destroy",):
             getattr(L, name).restype = ctypes.c_int

@@ -19,6 +19,7 @@
 
 #include "../../include/prost_b200.h"
 #include "prost_phases.cuh"
+#include "prost_resident.cuh"
 
 using namespace prost;
 
@@ -45,6 +46,14 @@ struct prost_handle {
   size_t esz = 4;
   int chunks = 1, nvmax = 0, wave = 0, n_ls = 0;
   Ops ops{};
+  // resident mode (k_resident): team geometry and its scratch
+  bool resident = false;
+  int rG = 0, rT = 0, rqpc = 0, rnt = 0;
+  size_t rsmem = 0;
+  unsigned* rbar = nullptr;
+  double* rpart = nullptr;
+  unsigned long long* rprof = nullptr;
+  int resident_ops_K = 0;
   // device state
   void* U = nullptr;
   void* r = nullptr;
@@ -215,6 +224,49 @@ struct Impl {
     h->launches += 1;
   }
 };
+
+// Register-resident frame kernel (prost_resident.cuh), fp32, one channel.
+struct ResOps {
+  cudaError_t (*launch)(const Args&, const RArgs&, int nt, size_t smem, cudaStream_t st);
+  cudaError_t (*prepare)(size_t smem);
+  int (*occupancy)(int nt, size_t smem);
+  size_t (*smem)(int qpc, int nwarp);
+  int ntmax;
+};
+
+template <int K, int NTMAX>
+struct Res {
+  static cudaError_t launch(const Args& a, const RArgs& ra, int nt, size_t smem, cudaStream_t st) {
+    Args aa = a;
+    RArgs rr = ra;
+    void* args[] = {&aa, &rr};
+    return cudaLaunchCooperativeKernel((const void*)k_resident<K, NTMAX>, dim3(ra.T * ra.G), dim3(nt),
+                                       args, smem, st);
+  }
+  static cudaError_t prepare(size_t smem) {
+    return cudaFuncSetAttribute(k_resident<K, NTMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+  }
+  static int occupancy(int nt, size_t smem) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_resident<K, NTMAX>, nt, smem) != cudaSuccess)
+      return 0;
+    return nb;
+  }
+  static size_t smem(int qpc, int nwarp) { return resident_smem<K>(qpc, nwarp); }
+};
+
+ResOps pick_resident(int K) {
+  switch (K) {
+    case 4: return ResOps{&Res<4, 768>::launch, &Res<4, 768>::prepare, &Res<4, 768>::occupancy, &Res<4, 768>::smem, 768};
+    case 8: return ResOps{&Res<8, 768>::launch, &Res<8, 768>::prepare, &Res<8, 768>::occupancy, &Res<8, 768>::smem, 768};
+    // 512 threads x 128 registers: the 60 basis registers of a 4-row group plus
+    // the CG working set (ptxas budgets registers per 128-thread granule)
+    case 15: return ResOps{&Res<15, 512>::launch, &Res<15, 512>::prepare, &Res<15, 512>::occupancy, &Res<15, 512>::smem, 512};
+    case 16: return ResOps{&Res<16, 512>::launch, &Res<16, 512>::prepare, &Res<16, 512>::occupancy, &Res<16, 512>::smem, 512};
+    default: return ResOps{nullptr, nullptr, nullptr, nullptr, 0};
+  }
+}
 
 template <typename T>
 Ops pick(int k) {
@@ -433,8 +485,47 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   ALLOC(cnt, S * sizeof(unsigned));
   ALLOC(rinv, S * KMAX * KMAX * sizeof(double));
   ALLOC(info, S * sizeof(FitInfo));
-#undef ALLOC
   CK(cudaMallocHost(&h->info_h, S * sizeof(FitInfo)));
+  // Resident frame kernel: fp32, one channel, k <= 16, and a team that fits the
+  // chip.  The geometry depends on the stream shape only (not on n_streams), so
+  // a stream's reduction order — and its result — is the same in any batch.
+  const char* no_res = getenv("PROST_NO_RESIDENT");
+  const ResOps ro = pick_resident(K);
+  if (!h->fp64 && h->C == 1 && ro.launch && !(no_res && no_res[0] == '1')) {
+    const int nq = h->Pp / 4;
+    int best_used = 0, best_qpc = 0;
+    for (int qpc = ro.ntmax / 4 * 4; qpc >= 32; qpc -= 4) {
+      const int G = (nq + qpc - 1) / qpc;
+      if (G > sms) break;
+      const int used = (sms / G) * G;
+      const int nt = (qpc + 31) / 32 * 32;
+      if (ro.smem(qpc, nt / 32) > 227 * 1024) continue;
+      // prefer full-chip use; among near-equal choices, the largest slice (fewest CTAs per team)
+      if (used > best_used * 1.03) {
+        best_used = used;
+        best_qpc = qpc;
+      }
+    }
+    if (best_qpc > 0) {
+      const int qpc = best_qpc;
+      const int nt = (qpc + 31) / 32 * 32;
+      const size_t sm = ro.smem(qpc, nt / 32);
+      if (ro.prepare(sm) == cudaSuccess && ro.occupancy(nt, sm) >= 1) {
+        h->resident = true;
+        h->rqpc = qpc;
+        h->rnt = nt;
+        h->rsmem = sm;
+        h->rG = (nq + qpc - 1) / qpc;
+        h->rT = std::min(h->S, sms / h->rG);
+        h->resident_ops_K = K;
+        ALLOC(rbar, (size_t)sms * sizeof(unsigned));
+        ALLOC(rpart, (size_t)2 * sms * RES_RNV_MAX * sizeof(double));
+        ALLOC(rprof, (size_t)sms * 8 * sizeof(unsigned long long));
+      }
+      cudaGetLastError();
+    }
+  }
+#undef ALLOC
   // U = first k unit vectors until the caller installs the numpy-drawn basis
   if (h->fp64) {
     std::vector<double> eye;
@@ -458,7 +549,8 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
 void prost_destroy(prost_handle* h) {
   if (!h) return;
   void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
-                  h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage};
+                  h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage,
+                  h->rbar, h->rpart, h->rprof};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->info_h) cudaFreeHost(h->info_h);
@@ -646,10 +738,30 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
     }
   }
   if (o.raw_mask && o.on_device && dense) a.raw_out = o.raw_mask;
-  const int wave = std::max(1, std::min(h->wave, h->S));
-  for (int s0 = 0; s0 < h->S; s0 += wave) {
-    a.s0 = s0;
-    h->ops.frame(h, a, st, std::min(wave, h->S - s0));
+  if (h->resident) {
+    // one cooperative launch for the whole frame of every stream, then the median
+    RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
+             h->prof ? h->rprof : nullptr};
+    CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * sizeof(unsigned), st));
+    long long n = 0;
+    {
+      PhaseTimer pt_(h, st, PROST_PH_FRAME);
+      CK(pick_resident(h->resident_ops_K).launch(a, ra, h->rnt, h->rsmem, st));
+      ++n;
+    }
+    if (a.mask_out) {
+      const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), h->S);
+      PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
+      k_median<<<mg, NT, 0, st>>>(a);
+      ++n;
+    }
+    h->launches += n;
+  } else {
+    const int wave = std::max(1, std::min(h->wave, h->S));
+    for (int s0 = 0; s0 < h->S; s0 += wave) {
+      a.s0 = s0;
+      h->ops.frame(h, a, st, std::min(wave, h->S - s0));
+    }
   }
   CK(cudaGetLastError());
   h->maybe_cold = false;
@@ -732,6 +844,9 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value) {
     case PROST_Q_BYTES_U: *value = (int64_t)h->k * h->np * (int64_t)h->esz; break;
     case PROST_Q_CHUNKS: *value = h->chunks; break;
     case PROST_Q_INSTANCE_K: *value = h->ops.K; break;
+    case PROST_Q_RESIDENT: *value = h->resident ? 1 : 0; break;
+    case PROST_Q_TEAM: *value = h->rG; break;
+    case PROST_Q_TEAMS: *value = h->rT; break;
     default: return fail(h, PROST_ERR_CONFIG, "unknown query %d", what);
   }
   return PROST_OK;
@@ -761,6 +876,27 @@ int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n
     if (launches) launches[i] = h->prof_n[i];
     h->prof_ms[i] = 0.0;
     h->prof_n[i] = 0;
+  }
+  return PROST_OK;
+}
+
+int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n) {
+  if (!h || !out) return PROST_ERR_CONFIG;
+  for (int i = 0; i < n; ++i) out[i] = 0;
+  if (!h->resident) return PROST_OK;
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  const int ctas = h->rT * h->rG;
+  std::vector<unsigned long long> v((size_t)ctas * 8);
+  CK(cudaMemcpy(v.data(), h->rprof, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  // per-CTA means of the counters of the last profiled launch, then the max total
+  for (int c = 0; c < ctas; ++c)
+    for (int i = 0; i < 8 && i < n; ++i) out[i] += (int64_t)v[(size_t)c * 8 + i];
+  for (int i = 0; i < 8 && i < n; ++i) out[i] /= ctas;
+  if (n > 8) {
+    unsigned long long mx = 0;
+    for (int c = 0; c < ctas; ++c) mx = std::max(mx, v[(size_t)c * 8]);
+    out[8] = (int64_t)mx;
   }
   return PROST_OK;
 }

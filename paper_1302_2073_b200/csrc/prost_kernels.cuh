@@ -285,7 +285,10 @@ __device__ __forceinline__ double alpha_at(const Args& a, int m) {
   return al;
 }
 
+static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied as 8-byte words");
+
 __device__ void write_info(Ctl* c, const Args& a, int s) {
+  if (!a.info) return;
   FitInfo fi;
   fi.fit_cost = c->f;
   fi.step = c->t;
@@ -397,6 +400,130 @@ __device__ void fail_iteration(Ctl* c, const Args& a, int s, int lane) {
   if (lane == 0) c->pend_alpha = 0.0;
   __syncwarp();
   finish_frame(c, a, s, lane);
+}
+
+__device__ __forceinline__ void mark_nonfinite(Ctl* c, const Args& a, int s, int lane) {
+  if (lane == 0) {
+    c->status = ST_NONFINITE;
+    c->active = 0;
+    c->t = step_size(a, c->frame_index);
+    write_info(c, a, s);
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Decisions after each reduction (warp 0; every lane sees the same `red`).
+// Shared by the streamed phase kernels and the resident frame kernel.
+
+// red: [0] cost, [1..K] sum_i U_ij g_i, [K+1] ||g||^2, [K+2] non-finite count
+template <int K>
+__device__ void after_pass0(Ctl* c, const Args& a, int s, int lane, const double* red) {
+  if (red[K + 2] > 0.0) { mark_nonfinite(c, a, s, lane); return; }
+  if (lane < a.k) {
+    const double gj = -red[1 + lane];  // fit.py:101: grad = -(U^T g)
+    c->grad[lane] = gj;
+    c->d[lane] = -gj;
+  }
+  if (lane == 0) {
+    c->f = red[0];
+    c->gsq = red[K + 1];
+    c->it = 0;
+    c->iterations = 0;
+    c->cost_evals = 1;
+    c->grad_evals = 1;
+    c->pend_alpha = 0.0;
+  }
+  __syncwarp();
+  begin_iteration(c, a, s, lane);
+}
+
+// red: [0..WC) trial costs, then per speculative slot mm: K gradient sums + ||g||^2
+template <int K>
+__device__ void after_iter(Ctl* c, const Args& a, int s, int lane, const double* red, int wlo) {
+  const int nmax = a.max_bt < WC ? a.max_bt : WC;
+  int first = -1;
+  double alpha = a.step0;
+  for (int m = 0; m < nmax; ++m) {
+    if (red[m] <= c->f + a.c_armijo * alpha * c->slope) {  // fit.py:126-135
+      first = m;
+      break;
+    }
+    alpha *= a.shrink;
+  }
+  if (lane == 0) c->pend_alpha = 0.0;
+  __syncwarp();
+  if (first >= 0) {
+    const int mm = first - wlo;
+    if (lane == 0) {
+      c->cost_evals += first + 1;
+      c->last_acc = first;
+    }
+    __syncwarp();
+    if (mm >= 0 && mm < WG) {
+      complete_iteration(c, a, s, lane, alpha, red[first], red + WC + mm * (K + 1),
+                         red[WC + mm * (K + 1) + K]);
+    } else if (lane == 0) {
+      c->need_gradfb = 1;
+      c->acc_idx = first;
+      c->acc_alpha = alpha;
+      c->acc_cost = red[first];
+    }
+  } else {
+    if (lane == 0) c->cost_evals += nmax;
+    __syncwarp();
+    if (nmax >= a.max_bt) {
+      fail_iteration(c, a, s, lane);
+    } else if (lane == 0) {
+      c->need_lsfb = 1;
+      c->ls_next = nmax;
+    }
+  }
+  __syncwarp();
+}
+
+// red: [0..cnt) trial costs for step indices base..base+cnt-1
+__device__ void after_lsfb(Ctl* c, const Args& a, int s, int lane, const double* red, int base) {
+  const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
+  int first = -1;
+  double alpha = alpha_at(a, base);
+  for (int m = 0; m < cnt; ++m) {
+    if (red[m] <= c->f + a.c_armijo * alpha * c->slope) {
+      first = m;
+      break;
+    }
+    alpha *= a.shrink;
+  }
+  if (first >= 0) {
+    if (lane == 0) {
+      c->cost_evals += first + 1;
+      c->need_lsfb = 0;
+      c->need_gradfb = 1;
+      c->last_acc = base + first;
+      c->acc_idx = base + first;
+      c->acc_alpha = alpha;
+      c->acc_cost = red[first];
+    }
+  } else {
+    if (lane == 0) c->cost_evals += cnt;
+    __syncwarp();
+    if (base + cnt >= a.max_bt) {
+      if (lane == 0) c->need_lsfb = 0;
+      __syncwarp();
+      fail_iteration(c, a, s, lane);
+    } else if (lane == 0) {
+      c->ls_next = base + cnt;
+    }
+  }
+  __syncwarp();
+}
+
+// red: [0..K) gradient sums at the accepted step, [K] ||g||^2
+template <int K>
+__device__ void after_gradfb(Ctl* c, const Args& a, int s, int lane, const double* red) {
+  if (lane == 0) c->need_gradfb = 0;
+  __syncwarp();
+  complete_iteration(c, a, s, lane, c->acc_alpha, c->acc_cost, red, red[K]);
 }
 
 }  // namespace prost

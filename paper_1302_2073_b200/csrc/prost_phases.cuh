@@ -270,32 +270,7 @@ __global__ void __launch_bounds__(NT) k_pass0(Args a) {
   cta_stage((double)gsq, sm, K + 1, NV);
   cta_stage(bad ? 1.0 : 0.0, sm, K + 2, NV);
   if (!cta_finish(a, s, sm, NV, red)) return;
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  if (red[K + 2] > 0.0) {
-    if (lane == 0) {
-      c->status = ST_NONFINITE;
-      c->t = step_size(a, c->frame_index);
-      write_info(c, a, s);
-    }
-    return;
-  }
-  if (lane < a.k) {
-    const double gj = -red[1 + lane];  // fit.py:101: grad = -(U^T g)
-    c->grad[lane] = gj;
-    c->d[lane] = -gj;
-  }
-  if (lane == 0) {
-    c->f = red[0];
-    c->gsq = red[K + 1];
-    c->it = 0;
-    c->iterations = 0;
-    c->cost_evals = 1;
-    c->grad_evals = 1;
-    c->pend_alpha = 0.0;
-  }
-  __syncwarp();
-  begin_iteration(c, a, s, lane);
+  if (threadIdx.x < 32) after_pass0<K>(c, a, s, threadIdx.x, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -408,47 +383,7 @@ __global__ void __launch_bounds__(NT) k_iter(Args a) {
     cta_stage((double)gsq[mm], sm, WC + mm * (K + 1) + K, NV);
   }
   if (!cta_finish(a, s, sm, NV, red)) return;
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  // First acceptable step in the window (fit.py:126-135), sequential semantics.
-  const int nmax = a.max_bt < WC ? a.max_bt : WC;
-  int first = -1;
-  double alpha = a.step0;
-  for (int m = 0; m < nmax; ++m) {
-    if (red[m] <= c->f + a.c_armijo * alpha * c->slope) {
-      first = m;
-      break;
-    }
-    alpha *= a.shrink;
-  }
-  if (lane == 0) c->pend_alpha = 0.0;  // applied by this kernel
-  __syncwarp();
-  if (first >= 0) {
-    const int mm = first - wlo;
-    if (lane == 0) {
-      c->cost_evals += first + 1;
-      c->last_acc = first;
-    }
-    __syncwarp();
-    if (mm >= 0 && mm < WG) {
-      complete_iteration(c, a, s, lane, alpha, red[first], red + WC + mm * (K + 1),
-                         red[WC + mm * (K + 1) + K]);
-    } else if (lane == 0) {
-      c->need_gradfb = 1;
-      c->acc_idx = first;
-      c->acc_alpha = alpha;
-      c->acc_cost = red[first];
-    }
-  } else {
-    if (lane == 0) c->cost_evals += nmax;
-    __syncwarp();
-    if (nmax >= a.max_bt) {
-      fail_iteration(c, a, s, lane);
-    } else if (lane == 0) {
-      c->need_lsfb = 1;
-      c->ls_next = nmax;
-    }
-  }
+  if (threadIdx.x < 32) after_iter<K>(c, a, s, threadIdx.x, red, wlo);
 }
 
 // ---------------------------------------------------------------------------
@@ -510,38 +445,7 @@ __global__ void __launch_bounds__(NT) k_lsfb(Args a) {
 #pragma unroll
   for (int m = 0; m < LSW; ++m) cta_stage(cost[m], sm, m, LSW);
   if (!cta_finish(a, s, sm, LSW, red)) return;
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  int first = -1;
-  double alpha = alpha_at(a, base);
-  for (int m = 0; m < cnt; ++m) {
-    if (red[m] <= c->f + a.c_armijo * alpha * c->slope) {
-      first = m;
-      break;
-    }
-    alpha *= a.shrink;
-  }
-  if (first >= 0) {
-    if (lane == 0) {
-      c->cost_evals += first + 1;
-      c->need_lsfb = 0;
-      c->need_gradfb = 1;
-      c->last_acc = base + first;
-      c->acc_idx = base + first;
-      c->acc_alpha = alpha;
-      c->acc_cost = red[first];
-    }
-  } else {
-    if (lane == 0) c->cost_evals += cnt;
-    __syncwarp();
-    if (base + cnt >= a.max_bt) {
-      if (lane == 0) c->need_lsfb = 0;
-      __syncwarp();
-      fail_iteration(c, a, s, lane);
-    } else if (lane == 0) {
-      c->ls_next = base + cnt;
-    }
-  }
+  if (threadIdx.x < 32) after_lsfb(c, a, s, threadIdx.x, red, base);
 }
 
 // ---------------------------------------------------------------------------
@@ -602,11 +506,7 @@ __global__ void __launch_bounds__(NT) k_gradfb(Args a) {
   for (int j = 0; j < K; ++j) cta_stage((double)acc[j], sm, j, NV);
   cta_stage((double)gsq, sm, K, NV);
   if (!cta_finish(a, s, sm, NV, red)) return;
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  if (lane == 0) c->need_gradfb = 0;
-  __syncwarp();
-  complete_iteration(c, a, s, lane, c->acc_alpha, c->acc_cost, red, red[K]);
+  if (threadIdx.x < 32) after_gradfb<K>(c, a, s, threadIdx.x, red);
 }
 
 // ---------------------------------------------------------------------------

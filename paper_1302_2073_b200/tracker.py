@@ -320,6 +320,15 @@ class NativeTracker:
         self._check(self._lib.prost_profile_read(self._h, nat.dptr(ms), cnt, n), "profile_read")
         return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(nat.PHASES)}
 
+    def resident_counters(self) -> dict:
+        """Per-CTA mean timings (us) of the last profiled resident launch."""
+        out = (ctypes.c_int64 * 9)()
+        self._check(self._lib.prost_resident_counters(self._h, out, 9), "resident_counters")
+        names = ("kernel_us", "barrier_us", "slots_us", "logic_us", "prefetch_us")
+        d = {nm: out[i] / 1e3 for i, nm in enumerate(names)}
+        d.update(team_sums=int(out[5]), rounds=int(out[6]), slowest_kernel_us=out[8] / 1e3)
+        return d
+
     def set_wave(self, streams: int) -> None:
         self._check(self._lib.prost_set_wave(self._h, streams), "set_wave")
 

@@ -110,7 +110,8 @@ def test_fit_cases(precision):
             assert [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z[key + "counts"])
 
 
-def test_periodic_reorthonormalization_fp64():
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_periodic_reorthonormalization(precision):
     """The unconditional QR at the 1000th geodesic step (manifold.py:192-196),
     replayed from the reference's state at step 997."""
     z = load("qr_chain")
@@ -126,9 +127,12 @@ def test_periodic_reorthonormalization_fp64():
     st = pkg.TrackerState(pkg.SubspaceBasis(ost.U, steps_since_qr=ost.since_qr), ost.y, ost.w,
                           frame_index=ost.frame_index)
     for i in range(998, 1003):
-        st, _, _ = pkg.process_frame(st, z["frames"][i], params, precision="fp64")
-        np.testing.assert_allclose(st.basis.data, z[f"U{i}"], rtol=0, atol=1e-10)
+        st, _, _ = pkg.process_frame(st, z["frames"][i], params, precision=precision)
+        np.testing.assert_allclose(st.basis.data, z[f"U{i}"], rtol=0,
+                                   atol=1e-10 if precision == "fp64" else 2e-5)
         assert st.basis.steps_since_qr == int(z[f"since{i}"])
+    U = st.basis.data
+    assert np.linalg.norm(U.T @ U - np.eye(3)) < (1e-12 if precision == "fp64" else 1e-5)
 
 
 def test_rejects_non_finite_frame_without_mutation():
@@ -307,3 +311,35 @@ def test_large_batch_properties():
     for s in range(S):
         U = bt.native.get_core_state(s)[0]
         assert np.linalg.norm(U.T @ U - np.eye(15)) < 1e-4
+
+
+def test_resident_kernel_is_the_product_path_and_matches_streamed(monkeypatch):
+    """C3 shape in fp32 runs in the register-resident frame kernel; the
+    multi-kernel streamed path (PROST_NO_RESIDENT=1) agrees with it."""
+    import torch
+    from paper_1302_2073_b200 import _native as nat
+
+    W, H, S, F = 320, 240, 6, 8
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=4, seed=0)
+    data = [c0_stream(F, W, H, seed=s) for s in range(S)]
+    out = {}
+    for mode in ("resident", "streamed"):
+        if mode == "streamed":
+            monkeypatch.setenv("PROST_NO_RESIDENT", "1")
+        bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        assert bt.native.query(nat.Q_RESIDENT) == (1 if mode == "resident" else 0)
+        mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
+        for f in range(F):
+            fr = torch.from_numpy(np.stack([d[f] for d in data]).astype(np.float32)).cuda()
+            info = bt.push(fr, background=bg, mask=mask, fit=True)
+        out[mode] = (mask.cpu().numpy(), bg.cpu().numpy(),
+                     [bt.native.get_core_state(s)[0] for s in range(S)],
+                     [info[s].fit_cost for s in range(S)])
+    (m1, b1, U1, c1), (m2, b2, U2, c2) = out["resident"], out["streamed"]
+    assert np.mean(m1 != m2) <= 0.001
+    assert np.linalg.norm(b1 - b2) <= 1e-5 * np.linalg.norm(b2)
+    for s in range(S):
+        assert sine(U1[s], U2[s]) <= 1e-4
+        assert c1[s] == pytest.approx(c2[s], rel=1e-5)
