@@ -234,36 +234,40 @@ struct ResOps {
   int ntmax;
 };
 
-template <int K, int NTMAX>
+template <int K, int NTMAX, int PM>
 struct Res {
   static cudaError_t launch(const Args& a, const RArgs& ra, int nt, size_t smem, cudaStream_t st) {
     Args aa = a;
     RArgs rr = ra;
     void* args[] = {&aa, &rr};
-    return cudaLaunchCooperativeKernel((const void*)k_resident<K, NTMAX>, dim3(ra.T * ra.G), dim3(nt),
-                                       args, smem, st);
+    return cudaLaunchCooperativeKernel((const void*)k_resident<K, NTMAX, PM>, dim3(ra.T * ra.G),
+                                       dim3(nt), args, smem, st);
   }
   static cudaError_t prepare(size_t smem) {
-    return cudaFuncSetAttribute(k_resident<K, NTMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem);
+    return cudaFuncSetAttribute(k_resident<K, NTMAX, PM>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   static int occupancy(int nt, size_t smem) {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_resident<K, NTMAX>, nt, smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_resident<K, NTMAX, PM>, nt, smem) !=
+        cudaSuccess)
       return 0;
     return nb;
   }
   static size_t smem(int qpc, int nwarp) { return resident_smem<K>(qpc, nwarp); }
+  static ResOps ops() { return ResOps{&launch, &prepare, &occupancy, &smem, NTMAX}; }
 };
 
-ResOps pick_resident(int K) {
+// p = 0.5 (every BASELINE config) gets its own instance with the two-RSQ
+// penalty; other exponents use the runtime-dispatched instance.
+// 512 threads x 128 registers for k <= 16: the 60 basis registers of a 4-row
+// group plus the CG working set (ptxas budgets registers per 128-thread granule).
+ResOps pick_resident(int K, bool half) {
   switch (K) {
-    case 4: return ResOps{&Res<4, 768>::launch, &Res<4, 768>::prepare, &Res<4, 768>::occupancy, &Res<4, 768>::smem, 768};
-    case 8: return ResOps{&Res<8, 768>::launch, &Res<8, 768>::prepare, &Res<8, 768>::occupancy, &Res<8, 768>::smem, 768};
-    // 512 threads x 128 registers: the 60 basis registers of a 4-row group plus
-    // the CG working set (ptxas budgets registers per 128-thread granule)
-    case 15: return ResOps{&Res<15, 512>::launch, &Res<15, 512>::prepare, &Res<15, 512>::occupancy, &Res<15, 512>::smem, 512};
-    case 16: return ResOps{&Res<16, 512>::launch, &Res<16, 512>::prepare, &Res<16, 512>::occupancy, &Res<16, 512>::smem, 512};
+    case 4: return half ? Res<4, 768, PM_HALF>::ops() : Res<4, 768, PM_ANY>::ops();
+    case 8: return half ? Res<8, 768, PM_HALF>::ops() : Res<8, 768, PM_ANY>::ops();
+    case 15: return half ? Res<15, 512, PM_HALF>::ops() : Res<15, 512, PM_ANY>::ops();
+    case 16: return half ? Res<16, 512, PM_HALF>::ops() : Res<16, 512, PM_ANY>::ops();
     default: return ResOps{nullptr, nullptr, nullptr, nullptr, 0};
   }
 }
@@ -490,7 +494,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   // chip.  The geometry depends on the stream shape only (not on n_streams), so
   // a stream's reduction order — and its result — is the same in any batch.
   const char* no_res = getenv("PROST_NO_RESIDENT");
-  const ResOps ro = pick_resident(K);
+  const ResOps ro = pick_resident(K, params->p == 0.5);
   if (!h->fp64 && h->C == 1 && ro.launch && !(no_res && no_res[0] == '1')) {
     const int nq = h->Pp / 4;
     int best_used = 0, best_qpc = 0;
@@ -746,7 +750,7 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
     long long n = 0;
     {
       PhaseTimer pt_(h, st, PROST_PH_FRAME);
-      CK(pick_resident(h->resident_ops_K).launch(a, ra, h->rnt, h->rsmem, st));
+      CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
       ++n;
     }
     if (a.mask_out) {

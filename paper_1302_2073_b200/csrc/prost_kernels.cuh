@@ -64,7 +64,7 @@ struct Ctl {
   long long pcount, pseen, frame_index, since_qr;
   int it, active, need_lsfb, need_gradfb, acc_idx, ls_next, gwin_lo, last_acc;
   int do_geo, qr_now, status, iterations, cost_evals, grad_evals, frozen, cold;
-  int update_stats, pad_;
+  int update_stats, no_info;  // no_info: this copy must not write FitInfo
 };
 
 struct FitInfo {  // layout-identical to prost_fit_info
@@ -180,30 +180,34 @@ template <typename T, int K> struct Vec {
 // smoothed lp penalty (cost.py:57-93): weighted term w*(r^2+mu)^(p/2) and the
 // residual gradient p*r*(w*term)/base.
 
-__device__ __forceinline__ void penalty(float r, float w, const Args& a, float& tw, float& g) {
+// PM: compile-time penalty mode, or PM_ANY for a runtime switch on a.pmode.
+constexpr int PM_ANY = -1;
+
+template <int PM>
+__device__ __forceinline__ void penalty_t(float r, float w, const Args& a, float& tw, float& g) {
   const float b = fmaf(r, r, (float)a.mu);
-  switch (a.pmode) {
-    case PM_HALF: {  // b^(1/4) and b^(-3/4) from two MUFU.RSQ
-      const float h = rsqrtf(b);
-      const float e = rsqrtf(h);
-      tw = e * w;
-      g = (float)a.p * r * tw * (h * h);
-    } break;
-    case PM_ONE: {
-      const float h = rsqrtf(b);
-      tw = b * h * w;
-      g = (float)a.p * r * w * h;
-    } break;
-    case PM_TWO:
-      tw = b * w;
-      g = (float)a.p * r * w;
-      break;
-    default: {
-      const float L = __log2f(b);
-      tw = exp2f((float)a.half_p * L) * w;
-      g = (float)a.p * r * tw * __frcp_rn(b);
-    } break;
+  const int pm = PM == PM_ANY ? a.pmode : PM;
+  if (pm == PM_HALF) {  // b^(1/4) and b^(-3/4) from two MUFU.RSQ
+    const float h = rsqrtf(b);
+    const float e = rsqrtf(h);
+    tw = e * w;
+    g = (float)a.p * r * tw * (h * h);
+  } else if (pm == PM_ONE) {
+    const float h = rsqrtf(b);
+    tw = b * h * w;
+    g = (float)a.p * r * w * h;
+  } else if (pm == PM_TWO) {
+    tw = b * w;
+    g = (float)a.p * r * w;
+  } else {
+    const float L = __log2f(b);
+    tw = exp2f((float)a.half_p * L) * w;
+    g = (float)a.p * r * tw * __frcp_rn(b);
   }
+}
+
+__device__ __forceinline__ void penalty(float r, float w, const Args& a, float& tw, float& g) {
+  penalty_t<PM_ANY>(r, w, a, tw, g);
 }
 
 // Double instantiation: the same operation sequence and rounding as the
@@ -287,8 +291,8 @@ __device__ __forceinline__ double alpha_at(const Args& a, int m) {
 
 static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied as 8-byte words");
 
-__device__ void write_info(Ctl* c, const Args& a, int s) {
-  if (!a.info) return;
+__device__ __noinline__ void write_info(Ctl* c, const Args& a, int s) {
+  if (!a.info || c->no_info) return;
   FitInfo fi;
   fi.fit_cost = c->f;
   fi.step = c->t;
@@ -302,7 +306,7 @@ __device__ void write_info(Ctl* c, const Args& a, int s) {
 
 // End of the CG loop: projected-gradient norm, geodesic scalars
 // (manifold.py:130-197, tracker.py:140-143).
-__device__ void finish_frame(Ctl* c, const Args& a, int s, int lane) {
+__device__ __noinline__ void finish_frame(Ctl* c, const Args& a, int s, int lane) {
   const double t = step_size(a, c->frame_index);
   const double gj = lane < a.k ? c->grad[lane] : 0.0;  // = U^T eta
   const double yj = lane < a.k ? c->y[lane] : 0.0;
@@ -335,7 +339,7 @@ __device__ void finish_frame(Ctl* c, const Args& a, int s, int lane) {
 }
 
 // Top of CG iteration c->it (fit.py:108-119).
-__device__ void begin_iteration(Ctl* c, const Args& a, int s, int lane) {
+__device__ __noinline__ void begin_iteration(Ctl* c, const Args& a, int s, int lane) {
   if (lane == 0) {
     c->need_lsfb = 0;
     c->need_gradfb = 0;
@@ -368,7 +372,7 @@ __device__ void begin_iteration(Ctl* c, const Args& a, int s, int lane) {
 
 // Accepted step alpha with cost fnew and coordinate-gradient sums gs[j]
 // (= sum_i U_ij g_i): fit.py:137-144.
-__device__ void complete_iteration(Ctl* c, const Args& a, int s, int lane, double alpha,
+__device__ __noinline__ void complete_iteration(Ctl* c, const Args& a, int s, int lane, double alpha,
                                    double fnew, const double* gs, double gsq_new) {
   const double dj = lane < a.k ? c->d[lane] : 0.0;
   const double gold = lane < a.k ? c->grad[lane] : 0.0;
@@ -395,7 +399,7 @@ __device__ void complete_iteration(Ctl* c, const Args& a, int s, int lane, doubl
   begin_iteration(c, a, s, lane);
 }
 
-__device__ void fail_iteration(Ctl* c, const Args& a, int s, int lane) {
+__device__ __noinline__ void fail_iteration(Ctl* c, const Args& a, int s, int lane) {
   // fit.py:133-134: no acceptable step -> leave the loop, residual unchanged
   if (lane == 0) c->pend_alpha = 0.0;
   __syncwarp();
@@ -418,7 +422,7 @@ __device__ __forceinline__ void mark_nonfinite(Ctl* c, const Args& a, int s, int
 
 // red: [0] cost, [1..K] sum_i U_ij g_i, [K+1] ||g||^2, [K+2] non-finite count
 template <int K>
-__device__ void after_pass0(Ctl* c, const Args& a, int s, int lane, const double* red) {
+__device__ __noinline__ void after_pass0(Ctl* c, const Args& a, int s, int lane, const double* red) {
   if (red[K + 2] > 0.0) { mark_nonfinite(c, a, s, lane); return; }
   if (lane < a.k) {
     const double gj = -red[1 + lane];  // fit.py:101: grad = -(U^T g)
@@ -440,7 +444,7 @@ __device__ void after_pass0(Ctl* c, const Args& a, int s, int lane, const double
 
 // red: [0..WC) trial costs, then per speculative slot mm: K gradient sums + ||g||^2
 template <int K>
-__device__ void after_iter(Ctl* c, const Args& a, int s, int lane, const double* red, int wlo) {
+__device__ __noinline__ void after_iter(Ctl* c, const Args& a, int s, int lane, const double* red, int wlo) {
   const int nmax = a.max_bt < WC ? a.max_bt : WC;
   int first = -1;
   double alpha = a.step0;
@@ -483,7 +487,7 @@ __device__ void after_iter(Ctl* c, const Args& a, int s, int lane, const double*
 }
 
 // red: [0..cnt) trial costs for step indices base..base+cnt-1
-__device__ void after_lsfb(Ctl* c, const Args& a, int s, int lane, const double* red, int base) {
+__device__ __noinline__ void after_lsfb(Ctl* c, const Args& a, int s, int lane, const double* red, int base) {
   const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
   int first = -1;
   double alpha = alpha_at(a, base);
@@ -520,7 +524,7 @@ __device__ void after_lsfb(Ctl* c, const Args& a, int s, int lane, const double*
 
 // red: [0..K) gradient sums at the accepted step, [K] ||g||^2
 template <int K>
-__device__ void after_gradfb(Ctl* c, const Args& a, int s, int lane, const double* red) {
+__device__ __noinline__ void after_gradfb(Ctl* c, const Args& a, int s, int lane, const double* red) {
   if (lane == 0) c->need_gradfb = 0;
   __syncwarp();
   complete_iteration(c, a, s, lane, c->acc_alpha, c->acc_cost, red, red[K]);

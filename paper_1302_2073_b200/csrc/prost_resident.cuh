@@ -138,7 +138,9 @@ __device__ __forceinline__ void team_sum(const RArgs& ra, int team, int rank, co
       const int v = v0 + i * nwarp;
       if (v < nv) {
         const double* b = area + (size_t)v * G;
-        for (int r = lane; r < G; r += 32) acc[i] += __ldcg(b + r);
+#pragma unroll
+        for (int c = 0; c < 5; ++c)  // G <= 160: up to 5 independent loads per lane
+          if (lane + 32 * c < G) acc[i] += __ldcg(b + lane + 32 * c);
       }
     }
 #pragma unroll
@@ -206,7 +208,7 @@ __host__ __device__ constexpr size_t resident_smem(int qpc, int nwarp) {
          (size_t)2 * K * K * 8 + 16;
 }
 
-template <int K, int NTMAX>
+template <int K, int NTMAX, int PM>
 __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
@@ -232,8 +234,6 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
   double* Rm = rinv + K * K;                          // [K*K]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(Rm + K * K);
 
-  Args la = a;
-  if (rank != 0) la.info = nullptr;  // one writer per stream
   unsigned epoch = 0;
   __shared__ unsigned long long sprof[8];
   if (tid < 8) sprof[tid] = 0;
@@ -297,6 +297,8 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
     }
     if (tid < (int)(sizeof(Ctl) / 8))
       reinterpret_cast<double*>(cs)[tid] = __ldcg(reinterpret_cast<const double*>(a.ctl + s) + tid);
+    __syncthreads();
+    if (tid == 0) cs->no_info = rank != 0;  // one FitInfo writer per stream
     __syncthreads();  // prefetch buffer consumed, control block staged
     if (tid == 0 && qcount > 0 && s + T < ra.S) {
       fence_proxy_async();
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
         if (red[2] > 0.0) {
           cs->status = ST_NONFINITE;
           cs->t = step_size(a, cs->frame_index);
-          write_info(cs, la, s);
+          write_info(cs, a, s);
         } else {
           cs->psum += red[0];
           cs->psumsq += red[1];
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
         rstage(bad ? 1.0 : 0.0, wred, K, K + 1);
         team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
         if (tid < 32) {
-          if (red[K] > 0.0) mark_nonfinite(cs, la, s, tid);
+          if (red[K] > 0.0) mark_nonfinite(cs, a, s, tid);
           else if (tid < k) cs->y[tid] = red[tid];
         }
         __syncthreads();
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
           for (int j = 0; j < K; ++j) uy += u[j][e] * (float)cs->y[j];
           r[e] = __fsub_rn(xh[e], uy);
           float tw;
-          penalty(r[e], weight(e), a, tw, g[e]);
+          penalty_t<PM>(r[e], weight(e), a, tw, g[e]);
           cost += (double)tw;
           pk[K] += g[e] * g[e];
         }
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
         stage_floats<K + 1>(pk, wred, K + 3, 1);
         rstage(bad ? 1.0 : 0.0, wred, K + 2, K + 3);
         team_sum(ra, team, rank, wred, K + 3, red, epoch, sprof);
-        LOGIC(after_pass0<K>(cs, la, s, tid, red));
+        LOGIC(after_pass0<K>(cs, a, s, tid, red));
         __syncthreads();
       }
 
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 float tw, g;
-                penalty(trial(r[e], (float)al, ud[e]), weight(e), a, tw, g);
+                penalty_t<PM>(trial(r[e], (float)al, ud[e]), weight(e), a, tw, g);
                 cost += (double)tw;
               }
             }
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
             al *= a.shrink;
           }
           team_sum(ra, team, rank, wred, LSW, red, epoch, sprof);
-          LOGIC(after_lsfb(cs, la, s, tid, red, base));
+          LOGIC(after_lsfb(cs, a, s, tid, red, base));
         } else if (cs->need_gradfb) {
           const float al = (float)cs->acc_alpha;
           float g[4], pk[K + 1];
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float tw;
-            penalty(trial(r[e], al, ud[e]), weight(e), a, tw, g[e]);
+            penalty_t<PM>(trial(r[e], al, ud[e]), weight(e), a, tw, g[e]);
             pk[K] += g[e] * g[e];
           }
 #pragma unroll
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
           }
           stage_floats<K + 1>(pk, wred, K + 1, 0);
           team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
-          LOGIC(after_gradfb<K>(cs, la, s, tid, red));
+          LOGIC(after_gradfb<K>(cs, a, s, tid, red));
         } else {
           constexpr int NV = WC + WG * (K + 1);
           const int wlo = cs->gwin_lo;
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               float tw, g;
-              penalty(trial(r[e], (float)al, ud[e]), weight(e), a, tw, g);
+              penalty_t<PM>(trial(r[e], (float)al, ud[e]), weight(e), a, tw, g);
               cost += (double)tw;
 #pragma unroll
               for (int mm = 0; mm < WG; ++mm)
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
           }
           stage_floats<WG * (K + 1)>(pk, wred, NV, WC);
           team_sum(ra, team, rank, wred, NV, red, epoch, sprof);
-          LOGIC(after_iter<K>(cs, la, s, tid, red, wlo));
+          LOGIC(after_iter<K>(cs, a, s, tid, red, wlo));
         }
         __syncthreads();
         // apply an accepted step to the register-resident residual
@@ -536,7 +538,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float tw, g;
-            penalty(r[e], weight(e), a, tw, g);
+            penalty_t<PM>(r[e], weight(e), a, tw, g);
             const float eta = -g;  // cost.py:103-112
             float uv = 0.f, ug = 0.f;
 #pragma unroll
