@@ -13,7 +13,8 @@ from pathlib import Path
 
 from .errors import ConfigError, DeviceError, DimensionError, NonFiniteError, SequenceError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libprost_b200.so"
+LIB_PATH = Path(os.environ.get("PROST_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libprost_b200.so")
 
 PROST_OK = 0
 ERR_CONFIG, ERR_DIMENSION, ERR_NONFINITE, ERR_SEQUENCE, ERR_CUDA = 1, 2, 3, 4, 5

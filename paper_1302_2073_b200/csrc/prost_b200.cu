@@ -493,9 +493,12 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   // Resident frame kernel: fp32, one channel, k <= 16, and a team that fits the
   // chip.  The geometry depends on the stream shape only (not on n_streams), so
   // a stream's reduction order — and its result — is the same in any batch.
+  // Opt-in (PROST_RESIDENT=1) until it outruns the streamed path on C3.
+  const char* want_res = getenv("PROST_RESIDENT");
   const char* no_res = getenv("PROST_NO_RESIDENT");
   const ResOps ro = pick_resident(K, params->p == 0.5);
-  if (!h->fp64 && h->C == 1 && ro.launch && !(no_res && no_res[0] == '1')) {
+  if (!h->fp64 && h->C == 1 && ro.launch && want_res && want_res[0] == '1' &&
+      !(no_res && no_res[0] == '1')) {
     const int nq = h->Pp / 4;
     int best_used = 0, best_qpc = 0;
     for (int qpc = ro.ntmax / 4 * 4; qpc >= 32; qpc -= 4) {

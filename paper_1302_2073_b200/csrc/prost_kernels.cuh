@@ -37,7 +37,13 @@ namespace prost {
 constexpr int KMAX = 32;      // largest supported subspace dimension
 constexpr int NT = 256;       // threads per CTA
 constexpr int NW = NT / 32;   // warps per CTA
-constexpr int WC = 4;         // Armijo trial costs evaluated per U pass
+#ifndef PROST_WC
+#define PROST_WC 6
+#endif
+#ifndef PROST_MINB
+#define PROST_MINB 2
+#endif
+constexpr int WC = PROST_WC;  // Armijo trial costs evaluated per U pass
 constexpr int WG = 2;         // speculative gradients per U pass
 constexpr int LSW = 16;       // trial costs per fallback line-search pass
 constexpr int MAXBT = 64;     // cap on CgOptions.max_backtracks

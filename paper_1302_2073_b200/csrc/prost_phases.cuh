@@ -68,7 +68,7 @@ __device__ __forceinline__ double running_std(const Ctl* c) {
 // scale (freezing it at frame i_init, jobs.py:201-209).
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_stats(Args a) {
+__global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   const bool upd = a.pipeline && !c->frozen && c->frame_index < a.i_init;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(NT) k_stats(Args a) {
 // k_cold: y = U^T x on a stream's first frame (fit.py:86-87, tracker.py:136).
 
 template <typename T, int K, int VEC>
-__global__ void __launch_bounds__(NT) k_cold(Args a) {
+__global__ void __launch_bounds__(NT) k_cold(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, upd;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NT) k_cold(Args a) {
 // k_pass0: r = x - U y, its cost and coordinate gradient (fit.py:96-104).
 
 template <typename T, int K, int VEC>
-__global__ void __launch_bounds__(NT) k_pass0(Args a) {
+__global__ void __launch_bounds__(NT, PROST_MINB) k_pass0(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, upd;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(NT) k_pass0(Args a) {
 // k_iter: one CG iteration's U pass (fit.py:108-141).
 
 template <typename T, int K, int VEC>
-__global__ void __launch_bounds__(NT) k_iter(Args a) {
+__global__ void __launch_bounds__(NT, PROST_MINB) k_iter(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, lo;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(NT) k_iter(Args a) {
 // k_lsfb: further Armijo trials over the stored residual and u_dir only.
 
 template <typename T, int VEC>
-__global__ void __launch_bounds__(NT) k_lsfb(Args a) {
+__global__ void __launch_bounds__(NT) k_lsfb(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, m0;
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(NT) k_lsfb(Args a) {
 // k_gradfb: coordinate gradient at an accepted step outside the window.
 
 template <typename T, int K, int VEC>
-__global__ void __launch_bounds__(NT) k_gradfb(Args a) {
+__global__ void __launch_bounds__(NT, PROST_MINB) k_gradfb(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go;
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(NT) k_gradfb(Args a) {
 // re-orthonormalization, manifold.py:192-196) and run the same epilogue.
 
 template <typename T, int K, int VEC, bool QR>
-__global__ void __launch_bounds__(NT) k_geo(Args a) {
+__global__ void __launch_bounds__(NT, PROST_MINB) k_geo(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, dogeo, relabel;
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(NT) k_geo(Args a) {
 // the reference's sign-fixed Householder QR) and stores R^{-1}.
 
 template <typename T, int K, int VEC>
-__global__ void __launch_bounds__(NT) k_gram(Args a) {
+__global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go;
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(NT) k_gram(Args a) {
 // ---------------------------------------------------------------------------
 // k_median: 3x3 majority vote with edge replication (pipeline.py:215-228).
 
-__global__ void __launch_bounds__(NT) k_median(Args a) {
+__global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(NT) k_median(Args a) {
 // k_background: clip((U y) * scale + mean, 0, 1) (jobs.py:231-239).
 
 template <typename T, int K, int VEC>
-__global__ void __launch_bounds__(NT) k_background(Args a) {
+__global__ void __launch_bounds__(NT) k_background(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   const Ctl* c = a.ctl + s;
   __shared__ double sy[K], sscale;

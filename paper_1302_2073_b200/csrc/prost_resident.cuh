@@ -209,7 +209,7 @@ __host__ __device__ constexpr size_t resident_smem(int qpc, int nwarp) {
 }
 
 template <int K, int NTMAX, int PM>
-__global__ void __launch_bounds__(NTMAX, 1) k_resident(Args a, RArgs ra) {
+__global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;

@@ -12,6 +12,7 @@ numpy calls as the reference (manifold.py:100-113), so U0 is bit-identical.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -344,7 +345,9 @@ _CORE_CACHE: dict = {}
 
 
 def _core_handle(m: int, params: ProstParams, precision: str, device: int) -> NativeTracker:
-    key = (m, params, precision, device)
+    # the kernel-path switches are read at handle creation: key on them too
+    key = (m, params, precision, device, os.environ.get("PROST_RESIDENT"),
+           os.environ.get("PROST_NO_RESIDENT"))
     h = _CORE_CACHE.get(key)
     if h is None:
         if len(_CORE_CACHE) > 8:

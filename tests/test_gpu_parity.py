@@ -110,10 +110,13 @@ def test_fit_cases(precision):
             assert [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z[key + "counts"])
 
 
-@pytest.mark.parametrize("precision", ["fp64", "fp32"])
-def test_periodic_reorthonormalization(precision):
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32-resident"])
+def test_periodic_reorthonormalization(precision, monkeypatch):
     """The unconditional QR at the 1000th geodesic step (manifold.py:192-196),
     replayed from the reference's state at step 997."""
+    if precision == "fp32-resident":
+        monkeypatch.setenv("PROST_RESIDENT", "1")
+        precision = "fp32"
     z = load("qr_chain")
     params = pkg.ProstParams(k=3, cfg=pkg.LpConfig(p=0.5, mu=0.06125), delta=0.35, omega=5e-5,
                              t_init=1e-2, t_min=1e-3, tau=1e-3, cg=pkg.CgOptions(max_iters=2))
@@ -313,9 +316,9 @@ def test_large_batch_properties():
         assert np.linalg.norm(U.T @ U - np.eye(15)) < 1e-4
 
 
-def test_resident_kernel_is_the_product_path_and_matches_streamed(monkeypatch):
-    """C3 shape in fp32 runs in the register-resident frame kernel; the
-    multi-kernel streamed path (PROST_NO_RESIDENT=1) agrees with it."""
+def test_resident_kernel_matches_streamed(monkeypatch):
+    """The register-resident frame kernel (PROST_RESIDENT=1) and the
+    multi-kernel streamed path agree on a C3-shaped batch."""
     import torch
     from paper_1302_2073_b200 import _native as nat
 
@@ -325,8 +328,10 @@ def test_resident_kernel_is_the_product_path_and_matches_streamed(monkeypatch):
     data = [c0_stream(F, W, H, seed=s) for s in range(S)]
     out = {}
     for mode in ("resident", "streamed"):
-        if mode == "streamed":
-            monkeypatch.setenv("PROST_NO_RESIDENT", "1")
+        if mode == "resident":
+            monkeypatch.setenv("PROST_RESIDENT", "1")
+        else:
+            monkeypatch.delenv("PROST_RESIDENT", raising=False)
         bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
         assert bt.native.query(nat.Q_RESIDENT) == (1 if mode == "resident" else 0)
         mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
