@@ -203,6 +203,25 @@ def cpu_model():
 # ---------------------------------------------------------------------------
 
 
+def shard_streams(rank, per_rank):
+    """Weak scaling by stream: rank r owns global streams
+    [r*per_rank, (r+1)*per_rank), each seeded by its global index; no data-path
+    collective."""
+    return list(range(rank * per_rank, (rank + 1) * per_rank))
+
+
+def reduce_max(value, world, device=None):
+    """Max over ranks of a per-rank device time (outside the timed region)."""
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -266,7 +285,7 @@ def main():
     P = W * H
     n = P * ch
     k = cfg.subspace_dim
-    stream_ids = list(range(rank * S, (rank + 1) * S))
+    stream_ids = shard_streams(rank, S)
 
     t_gen = time.perf_counter()
     host = gen_frames(args.config, stream_ids, args.frames)  # [F, S, n] float32
@@ -296,13 +315,7 @@ def main():
             dist.barrier()
 
     def max_over_ranks(v):
-        if ws == 1:
-            return v
-        import torch.distributed as dist
-
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(v, ws, f"cuda:{dev}")
 
     step = 0
     preroll = cfg.i_init if args.preroll is None else args.preroll
