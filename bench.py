@@ -296,8 +296,10 @@ def main():
         bt.native.set_wave(args.wave)
     from paper_1302_2073_b200 import _native as nat
 
-    if bt.native.query(nat.Q_RESIDENT):
-        kernel_path = (f"resident: {bt.native.query(nat.Q_TEAMS)} teams x "
+    mode = bt.native.query(nat.Q_RESIDENT)
+    if mode:
+        kernel_path = (f"{'tmem' if mode == 2 else 'register'}-resident: "
+                       f"{bt.native.query(nat.Q_TEAMS)} teams x "
                        f"{bt.native.query(nat.Q_TEAM)} CTAs, one cooperative launch per step")
     else:
         kernel_path = f"streamed: {bt.native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel"

@@ -148,7 +148,7 @@ int prost_last_error(prost_handle* h, char* buf, int32_t len);
 #define PROST_Q_BYTES_U 2
 #define PROST_Q_CHUNKS 3
 #define PROST_Q_INSTANCE_K 4
-#define PROST_Q_RESIDENT 5   /* 1 when frames run in the register-resident kernel */
+#define PROST_Q_RESIDENT 5   /* 0 streamed, 1 register-resident, 2 TMEM-resident kernel */
 #define PROST_Q_TEAM 6       /* CTAs per team (resident mode) */
 #define PROST_Q_TEAMS 7      /* teams (resident mode) */
 int prost_query(prost_handle* h, int32_t what, int64_t* value);

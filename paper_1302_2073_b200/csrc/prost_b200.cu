@@ -20,6 +20,7 @@
 #include "../../include/prost_b200.h"
 #include "prost_phases.cuh"
 #include "prost_resident.cuh"
+#include "prost_tmem.cuh"
 
 using namespace prost;
 
@@ -30,6 +31,7 @@ namespace {
 struct Ops {
   void (*frame)(prost_handle*, Args&, cudaStream_t, int sw);
   void (*background)(prost_handle*, Args&, cudaStream_t, int sw);
+  void (*qr)(prost_handle*, Args&, cudaStream_t, int sw);  // periodic QR pair only
   int K, VEC;
 };
 
@@ -46,8 +48,9 @@ struct prost_handle {
   size_t esz = 4;
   int chunks = 1, nvmax = 0, wave = 0, n_ls = 0;
   Ops ops{};
-  // resident mode (k_resident): team geometry and its scratch
+  // resident modes (k_resident / k_tmem): team geometry and its scratch
   bool resident = false;
+  bool tmem = false;
   int rG = 0, rT = 0, rqpc = 0, rnt = 0;
   size_t rsmem = 0;
   unsigned* rbar = nullptr;
@@ -219,6 +222,14 @@ struct Impl {
     h->launches += n;
   }
 
+  static void qr(prost_handle* h, Args& a, cudaStream_t st, int sw) {
+    const dim3 grid(h->chunks, sw);
+    long long n = 0;
+    LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
+    h->launches += n;
+  }
+
   static void background(prost_handle* h, Args& a, cudaStream_t st, int sw) {
     k_background<T, K, VEC><<<dim3(h->chunks, sw), NT, 0, st>>>(a);
     h->launches += 1;
@@ -272,10 +283,52 @@ ResOps pick_resident(int K, bool half) {
   }
 }
 
+// TMEM-resident frame kernel (prost_tmem.cuh), fp32, one channel, k <= 16.
+struct TmOps {
+  cudaError_t (*launch)(const Args&, const RArgs&, size_t smem, cudaStream_t st);
+  cudaError_t (*prepare)(size_t smem);
+  int (*occupancy)(size_t smem);
+  size_t (*smem)(int qpc);
+  int qt;  // row groups per thread held in TMEM
+};
+
+template <int K, int PM>
+struct Tm {
+  static cudaError_t launch(const Args& a, const RArgs& ra, size_t smem, cudaStream_t st) {
+    Args aa = a;
+    RArgs rr = ra;
+    void* args[] = {&aa, &rr};
+    return cudaLaunchCooperativeKernel((const void*)k_tmem<K, PM>, dim3(ra.T * ra.G), dim3(TM_NT),
+                                       args, smem, st);
+  }
+  static cudaError_t prepare(size_t smem) {
+    return cudaFuncSetAttribute(k_tmem<K, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  static int occupancy(size_t smem) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tmem<K, PM>, TM_NT, smem) != cudaSuccess)
+      return 0;
+    return nb;
+  }
+  static size_t smem(int qpc) { return tmem_smem<K>(qpc); }
+  static TmOps ops() { return TmOps{&launch, &prepare, &occupancy, &smem, TmemGeom<K>::QT}; }
+};
+
+TmOps pick_tmem(int K, bool half) {
+  switch (K) {
+    case 4: return half ? Tm<4, PM_HALF>::ops() : Tm<4, PM_ANY>::ops();
+    case 8: return half ? Tm<8, PM_HALF>::ops() : Tm<8, PM_ANY>::ops();
+    case 15: return half ? Tm<15, PM_HALF>::ops() : Tm<15, PM_ANY>::ops();
+    case 16: return half ? Tm<16, PM_HALF>::ops() : Tm<16, PM_ANY>::ops();
+    default: return TmOps{nullptr, nullptr, nullptr, nullptr, 0};
+  }
+}
+
 template <typename T>
 Ops pick(int k) {
 #define PROST_K(KK) \
-  if (k <= KK) return Ops{&Impl<T, KK>::frame, &Impl<T, KK>::background, KK, Impl<T, KK>::VEC};
+  if (k <= KK) \
+    return Ops{&Impl<T, KK>::frame, &Impl<T, KK>::background, &Impl<T, KK>::qr, KK, Impl<T, KK>::VEC};
   PROST_K(4)
   PROST_K(8)
   PROST_K(15)
@@ -284,7 +337,7 @@ Ops pick(int k) {
   PROST_K(30)
   PROST_K(32)
 #undef PROST_K
-  return Ops{nullptr, nullptr, 0, 0};
+  return Ops{nullptr, nullptr, nullptr, 0, 0};
 }
 
 int validate(prost_handle* h, const prost_params* p, int n_streams) {
@@ -493,12 +546,41 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   // Resident frame kernel: fp32, one channel, k <= 16, and a team that fits the
   // chip.  The geometry depends on the stream shape only (not on n_streams), so
   // a stream's reduction order — and its result — is the same in any batch.
-  // Opt-in (PROST_RESIDENT=1) until it outruns the streamed path on C3.
+  // Kernel path: PROST_KERNEL = streamed | resident | tmem (PROST_RESIDENT=1 is
+  // an alias of resident; PROST_NO_RESIDENT=1 forces streamed).
   const char* want_res = getenv("PROST_RESIDENT");
   const char* no_res = getenv("PROST_NO_RESIDENT");
+  const char* kenv = getenv("PROST_KERNEL");
+  std::string kpath = kenv ? kenv : (want_res && want_res[0] == '1' ? "resident" : "tmem");
+  if (no_res && no_res[0] == '1') kpath = "streamed";
+  const bool eligible = !h->fp64 && h->C == 1 && K <= 16;
+  const TmOps to = pick_tmem(K, params->p == 0.5);
+  if (eligible && kpath == "tmem" && to.launch) {
+    // smallest team whose slice fits TMEM + shared memory: the most streams in flight
+    const int nq = h->Pp / 4;
+    for (int G = 1; G <= sms; ++G) {
+      const int qpc = ((nq + G - 1) / G + 3) / 4 * 4;
+      if ((nq + qpc - 1) / qpc != G) continue;
+      const size_t sm = to.smem(qpc);
+      if (sm > 227 * 1024) continue;
+      if (to.prepare(sm) == cudaSuccess && to.occupancy(sm) >= 1) {
+        h->tmem = true;
+        h->rqpc = qpc;
+        h->rnt = TM_NT;
+        h->rsmem = sm;
+        h->rG = G;
+        h->rT = std::min(h->S, sms / G);
+        h->resident_ops_K = K;
+        ALLOC(rbar, (size_t)sms * sizeof(unsigned));
+        ALLOC(rpart, (size_t)2 * sms * RES_RNV_MAX * sizeof(double));
+        ALLOC(rprof, (size_t)sms * 8 * sizeof(unsigned long long));
+      }
+      cudaGetLastError();
+      break;
+    }
+  }
   const ResOps ro = pick_resident(K, params->p == 0.5);
-  if (!h->fp64 && h->C == 1 && ro.launch && want_res && want_res[0] == '1' &&
-      !(no_res && no_res[0] == '1')) {
+  if (eligible && ro.launch && kpath == "resident") {
     const int nq = h->Pp / 4;
     int best_used = 0, best_qpc = 0;
     for (int qpc = ro.ntmax / 4 * 4; qpc >= 32; qpc -= 4) {
@@ -745,7 +827,7 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
     }
   }
   if (o.raw_mask && o.on_device && dense) a.raw_out = o.raw_mask;
-  if (h->resident) {
+  if (h->resident || h->tmem) {
     // one cooperative launch for the whole frame of every stream, then the median
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
              h->prof ? h->rprof : nullptr};
@@ -753,9 +835,13 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
     long long n = 0;
     {
       PhaseTimer pt_(h, st, PROST_PH_FRAME);
-      CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
+      if (h->tmem)
+        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rsmem, st));
+      else
+        CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
       ++n;
     }
+    if (h->tmem) h->ops.qr(h, a, st, h->S);  // exits at once unless a QR is due
     if (a.mask_out) {
       const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), h->S);
       PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
@@ -851,7 +937,7 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value) {
     case PROST_Q_BYTES_U: *value = (int64_t)h->k * h->np * (int64_t)h->esz; break;
     case PROST_Q_CHUNKS: *value = h->chunks; break;
     case PROST_Q_INSTANCE_K: *value = h->ops.K; break;
-    case PROST_Q_RESIDENT: *value = h->resident ? 1 : 0; break;
+    case PROST_Q_RESIDENT: *value = h->tmem ? 2 : (h->resident ? 1 : 0); break;
     case PROST_Q_TEAM: *value = h->rG; break;
     case PROST_Q_TEAMS: *value = h->rT; break;
     default: return fail(h, PROST_ERR_CONFIG, "unknown query %d", what);
@@ -890,7 +976,7 @@ int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n
 int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n) {
   if (!h || !out) return PROST_ERR_CONFIG;
   for (int i = 0; i < n; ++i) out[i] = 0;
-  if (!h->resident) return PROST_OK;
+  if (!h->resident && !h->tmem) return PROST_OK;
   CK(cudaSetDevice(h->device));
   CK(cudaDeviceSynchronize());
   const int ctas = h->rT * h->rG;

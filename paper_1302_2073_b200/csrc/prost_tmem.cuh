@@ -1,0 +1,536 @@
+// prost_tmem.cuh — the TMEM-resident frame kernel (k_tmem).
+//
+// Same team structure as k_resident (a persistent cooperative grid split into
+// T teams of G CTAs; a team owns one stream per round; the frame's dependent
+// reductions are team-wide sums through double-buffered global slots and a
+// release/acquire counter barrier, after which every CTA runs the scalar
+// logic itself).  The difference is where a CTA keeps its slice of U: each
+// thread owns QT row groups (4 rows x k columns each) in its lane of tensor
+// memory (tcgen05.st once per frame, tcgen05.ld in every phase) plus, when the
+// slice is larger, one more group in shared memory.  With 256 KB of TMEM +
+// shared memory per SM a C3 stream (76,800 x 15 fp32 = 4.6 MB) fits on 14
+// SMs, so ~10 streams are in flight at once — enough to cover the latency of
+// the reduction chain — and U still crosses HBM exactly once each way.
+#pragma once
+
+#include "prost_resident.cuh"
+#include "tmem_io.cuh"
+
+namespace prost {
+
+constexpr int TM_NT = 512;  // threads per CTA: 16 warps = 4 per TMEM lane quarter
+
+template <int K>
+struct TmemGeom {
+  static constexpr int QCOLS = 4 * K;  // TMEM columns per row group
+  // column stride between a thread's row groups: a power of two, so every
+  // tcgen05 access (x32/x16/x8/x4) starts at a column aligned to its width
+  static constexpr int STRIDE = QCOLS <= 16 ? 16 : (QCOLS <= 32 ? 32 : 64);
+  static constexpr int QT = 128 / STRIDE;  // row groups per thread in TMEM
+};
+
+// Dynamic shared memory of k_tmem<K> for qpc row groups per CTA.
+template <int K>
+__host__ __device__ constexpr size_t tmem_smem(int qpc) {
+  const int qs = qpc > TmemGeom<K>::QT * TM_NT ? qpc - TmemGeom<K>::QT * TM_NT : 0;
+  return (size_t)K * qs * 16                    // basis row groups kept in shared memory
+         + (size_t)qpc * (4 * 16 + 4)           // r, u_dir, normalized frame, mean, labels
+         + (size_t)(TM_NT / 32 + 1) * RES_RNV_MAX * 8 + sizeof(Ctl) + 64;
+}
+
+template <int K, int PM>
+__global__ void __launch_bounds__(TM_NT, 1)
+    k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
+  using Geo = TmemGeom<K>;
+  constexpr int QC = Geo::QCOLS, QT = Geo::QT, QS = Geo::STRIDE;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ unsigned s_tbase;
+  __shared__ unsigned long long sprof[8];
+  const int G = ra.G, T = ra.T, qpc = ra.qpc;
+  const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int k = a.k;
+  const int nq = a.Pp / 4;
+  const int q0 = rank * qpc;
+  const int qcount = max(0, min(qpc, nq - q0));
+  const int nslots = (qcount + TM_NT - 1) / TM_NT;  // uniform across the CTA
+  const int qs = qpc > QT * TM_NT ? qpc - QT * TM_NT : 0;
+
+  float4* sU = reinterpret_cast<float4*>(smem_raw);  // [K][qs]
+  float4* sR = sU + (size_t)K * qs;                  // [qpc] residual
+  float4* sD = sR + qpc;                             // [qpc] u_dir
+  float4* sX = sD + qpc;                             // [qpc] normalized frame
+  float4* sM = sX + qpc;                             // [qpc] running mean
+  uint32_t* sL = reinterpret_cast<uint32_t*>(sM + qpc);  // [qpc] label bytes
+  double* wred = reinterpret_cast<double*>(sL + ((qpc + 1) / 2) * 2);
+  double* red = wred + (size_t)(TM_NT / 32) * RES_RNV_MAX;
+  Ctl* cs = reinterpret_cast<Ctl*>(red + RES_RNV_MAX);
+
+  if (tid < 8) sprof[tid] = 0;
+  const unsigned long long t_start = gtimer();
+  // TMEM: 512 columns, allocated by warp 0
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_addr(&s_tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // this thread's lane and columns: lane quarter = warp % 4, column block = warp / 4
+  const unsigned tbase = s_tbase + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 128);
+  unsigned epoch = 0;
+
+#define LOGIC(call)                                                        \
+  do {                                                                     \
+    const unsigned long long tl0 = (ra.prof && tid == 0) ? gtimer() : 0;   \
+    if (tid < 32) call;                                                    \
+    if (ra.prof && tid == 0) sprof[PROF_LOGIC] += gtimer() - tl0;          \
+  } while (0)
+
+  // row group (slot) -> basis registers
+  auto load_u = [&](int slot, float* u) {
+    if (slot < QT) {
+      tmem_ld<QC>(tbase + slot * QS, u);
+      tmem_wait_ld();
+    } else {
+      const int i = slot * TM_NT + tid - QT * TM_NT;
+      const bool ok = slot * TM_NT + tid < qcount;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const float4 t = ok ? sU[(size_t)j * qs + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        u[4 * j + 0] = t.x; u[4 * j + 1] = t.y; u[4 * j + 2] = t.z; u[4 * j + 3] = t.w;
+      }
+    }
+  };
+  auto store_u_onchip = [&](int slot, const float* u) {
+    if (slot < QT) {
+      tmem_st<QC>(tbase + slot * QS, u);
+    } else if (slot * TM_NT + tid < qcount) {
+      const int i = slot * TM_NT + tid - QT * TM_NT;
+#pragma unroll
+      for (int j = 0; j < K; ++j) sU[(size_t)j * qs + i] = make_float4(u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+    }
+  };
+  auto f4 = [](float4 v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; };
+
+  for (int s = team; s < ra.S; s += T) {
+    if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
+    // ---- load this stream's slice: U -> TMEM / shared, frame, mean, labels ---
+    {
+      const unsigned long long tw0 = (ra.prof && tid == 0) ? gtimer() : 0;
+      const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
+      for (int slot = 0; slot < nslots; ++slot) {
+        const int qi = slot * TM_NT + tid;  // row group within the slice
+        const bool ok = qi < qcount;
+        const size_t off = (size_t)(q0 + qi) * 4;
+        float u[QC];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ok && j < k) t = __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + off));
+          u[4 * j] = t.x; u[4 * j + 1] = t.y; u[4 * j + 2] = t.z; u[4 * j + 3] = t.w;
+        }
+        store_u_onchip(slot, u);
+        if (ok) {
+          sX[qi] = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + (size_t)s * a.np + off));
+          sM[qi] = a.pipeline ? *reinterpret_cast<const float4*>(static_cast<const float*>(a.mean) + (size_t)s * a.np + off)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          sL[qi] = *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + (q0 + qi) * 4);
+        }
+      }
+      tmem_wait_st();
+      if (tid < (int)(sizeof(Ctl) / 8))
+        reinterpret_cast<double*>(cs)[tid] = __ldcg(reinterpret_cast<const double*>(a.ctl + s) + tid);
+      __syncthreads();
+      if (tid == 0) cs->no_info = rank != 0;
+      __syncthreads();
+      if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += gtimer() - tw0;
+    }
+    const float omega = (float)a.omega;
+    auto weights = [&](int qi, float* w) {
+      const uint32_t lb = qi < qcount ? sL[qi] : 0u;
+      const int pix = (q0 + qi) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = (qi < qcount && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
+    };
+
+    // ---- frame start: running statistics (pipeline.py:120-140) -------------
+    const bool upd = a.pipeline && !cs->frozen && cs->frame_index < a.i_init;
+    if (upd) {
+      double s1 = 0.0, s2 = 0.0, nf = 0.0;
+      for (int slot = 0; slot < nslots; ++slot) {
+        const int qi = slot * TM_NT + tid;
+        if (qi >= qcount) continue;
+        float xv[4];
+        f4(sX[qi], xv);
+        const int pix = (q0 + qi) * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (pix + e < a.P) {
+            const double v = (double)xv[e];
+            s1 += v;
+            s2 += v * v;
+            nf += isfinite(v) ? 0.0 : 1.0;
+          }
+        }
+      }
+      rstage(s1, wred, 0, 3);
+      rstage(s2, wred, 1, 3);
+      rstage(nf, wred, 2, 3);
+      team_sum(ra, team, rank, wred, 3, red, epoch, sprof);
+      if (tid == 0) {
+        if (red[2] > 0.0) {
+          cs->status = ST_NONFINITE;
+          cs->t = step_size(a, cs->frame_index);
+          write_info(cs, a, s);
+        } else {
+          cs->psum += red[0];
+          cs->psumsq += red[1];
+          cs->pcount += a.n_real;
+          cs->pseen += 1;
+          cs->std_cur = running_std(cs);
+          cs->update_stats = 1;
+          cs->status = ST_OK;
+        }
+      }
+    } else if (tid == 0) {
+      double sd = 1.0;
+      if (a.pipeline) {
+        sd = cs->frozen ? cs->pstd : running_std(cs);
+        if (!cs->frozen) {
+          cs->frozen = 1;
+          cs->pstd = sd;
+        }
+      }
+      cs->std_cur = sd;
+      cs->update_stats = 0;
+      cs->status = ST_OK;
+    }
+    __syncthreads();
+
+    // normalize the frame in place; fold the running mean (pipeline.py:148-156)
+    bool bad = false;
+    if (cs->status == ST_OK) {
+      const float stdv = (float)cs->std_cur, seen = (float)cs->pseen;
+      for (int slot = 0; slot < nslots; ++slot) {
+        const int qi = slot * TM_NT + tid;
+        if (qi >= qcount) continue;
+        const int pix = (q0 + qi) * 4;
+        float xv[4], mv[4], xh[4];
+        f4(sX[qi], xv);
+        f4(sM[qi], mv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bad |= !isfinite(xv[e]);
+          if (a.pipeline) {
+            if (upd) mv[e] = __fadd_rn(mv[e], __fdiv_rn(__fsub_rn(xv[e], mv[e]), seen));
+            xh[e] = __fdiv_rn(__fsub_rn(xv[e], mv[e]), stdv);
+          } else {
+            xh[e] = xv[e];
+          }
+          if (pix + e >= a.P) xh[e] = 0.f;
+        }
+        sX[qi] = make_float4(xh[0], xh[1], xh[2], xh[3]);
+        if (upd) {
+          sM[qi] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + (size_t)s * a.np + pix) = sM[qi];
+        }
+      }
+
+      // ---- cold start y = U^T x (fit.py:86-87) -------------------------------
+      if (cs->frame_index == 0) {
+        float pk[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) pk[j] = 0.f;
+        for (int slot = 0; slot < nslots; ++slot) {
+          const int qi = slot * TM_NT + tid;
+          float u[QC], xh[4];
+          load_u(slot, u);
+          f4(qi < qcount ? sX[qi] : make_float4(0.f, 0.f, 0.f, 0.f), xh);
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk[j] += u[4 * j + e] * xh[e];
+        }
+        stage_floats<K>(pk, wred, K + 1, 0);
+        rstage(bad ? 1.0 : 0.0, wred, K, K + 1);
+        team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
+        if (tid < 32) {
+          if (red[K] > 0.0) mark_nonfinite(cs, a, s, tid);
+          else if (tid < k) cs->y[tid] = red[tid];
+        }
+        __syncthreads();
+      }
+    }
+
+    if (cs->status == ST_OK) {
+      // ---- pass 0: r = x - U y, cost, coordinate gradient (fit.py:96-104) ---
+      {
+        double cost = 0.0;
+        float pk[K + 1];
+#pragma unroll
+        for (int j = 0; j <= K; ++j) pk[j] = 0.f;
+        for (int slot = 0; slot < nslots; ++slot) {
+          const int qi = slot * TM_NT + tid;
+          float u[QC], xh[4], w[4], r[4], g[4];
+          load_u(slot, u);
+          f4(qi < qcount ? sX[qi] : make_float4(0.f, 0.f, 0.f, 0.f), xh);
+          weights(qi, w);
+          float tc = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float uy = 0.f;
+#pragma unroll
+            for (int j = 0; j < K; ++j) uy += u[4 * j + e] * (float)cs->y[j];
+            r[e] = __fsub_rn(xh[e], uy);
+            float tw;
+            penalty_t<PM>(r[e], w[e], a, tw, g[e]);
+            tc += tw;
+            pk[K] += g[e] * g[e];
+          }
+          cost += (double)tc;
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pk[j] += u[4 * j + e] * g[e];
+          if (qi < qcount) sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
+        }
+        rstage(cost, wred, 0, K + 3);
+        stage_floats<K + 1>(pk, wred, K + 3, 1);
+        rstage(bad ? 1.0 : 0.0, wred, K + 2, K + 3);
+        team_sum(ra, team, rank, wred, K + 3, red, epoch, sprof);
+        LOGIC(after_pass0<K>(cs, a, s, tid, red));
+        __syncthreads();
+      }
+
+      // ---- CG iterations (fit.py:108-144) -----------------------------------
+      while (cs->status == ST_OK && cs->active) {
+        if (cs->need_lsfb) {
+          const int base = cs->ls_next;
+          const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
+          const double al0 = alpha_at(a, base);
+          float cst[LSW];
+#pragma unroll
+          for (int m = 0; m < LSW; ++m) cst[m] = 0.f;
+          for (int slot = 0; slot < nslots; ++slot) {
+            const int qi = slot * TM_NT + tid;
+            if (qi >= qcount) continue;
+            float r[4], ud[4], w[4];
+            f4(sR[qi], r);
+            f4(sD[qi], ud);
+            weights(qi, w);
+            double al = al0;
+#pragma unroll
+            for (int m = 0; m < LSW; ++m) {
+              if (m < cnt) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float tw, g;
+                  penalty_t<PM>(trial(r[e], (float)al, ud[e]), w[e], a, tw, g);
+                  cst[m] += tw;
+                }
+              }
+              al *= a.shrink;
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < LSW; ++m) rstage((double)cst[m], wred, m, LSW);
+          team_sum(ra, team, rank, wred, LSW, red, epoch, sprof);
+          LOGIC(after_lsfb(cs, a, s, tid, red, base));
+        } else if (cs->need_gradfb) {
+          const float al = (float)cs->acc_alpha;
+          float pk[K + 1];
+#pragma unroll
+          for (int j = 0; j <= K; ++j) pk[j] = 0.f;
+          for (int slot = 0; slot < nslots; ++slot) {
+            const int qi = slot * TM_NT + tid;
+            float u[QC], r[4], ud[4], w[4], g[4];
+            load_u(slot, u);
+            f4(qi < qcount ? sR[qi] : make_float4(0.f, 0.f, 0.f, 0.f), r);
+            f4(qi < qcount ? sD[qi] : make_float4(0.f, 0.f, 0.f, 0.f), ud);
+            weights(qi, w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float tw;
+              penalty_t<PM>(trial(r[e], al, ud[e]), w[e], a, tw, g[e]);
+              pk[K] += g[e] * g[e];
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pk[j] += u[4 * j + e] * g[e];
+          }
+          stage_floats<K + 1>(pk, wred, K + 1, 0);
+          team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
+          LOGIC(after_gradfb<K>(cs, a, s, tid, red));
+        } else {
+          constexpr int NV = WC + WG * (K + 1);
+          const int wlo = cs->gwin_lo;
+          float cst[WC];
+          float pk[WG * (K + 1)];
+#pragma unroll
+          for (int m = 0; m < WC; ++m) cst[m] = 0.f;
+#pragma unroll
+          for (int i = 0; i < WG * (K + 1); ++i) pk[i] = 0.f;
+          for (int slot = 0; slot < nslots; ++slot) {
+            const int qi = slot * TM_NT + tid;
+            float u[QC], r[4], ud[4], w[4];
+            load_u(slot, u);
+            f4(qi < qcount ? sR[qi] : make_float4(0.f, 0.f, 0.f, 0.f), r);
+            weights(qi, w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ud[e] = 0.f;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              const float dj = (float)cs->d[j];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) ud[e] += u[4 * j + e] * dj;
+            }
+            if (qi < qcount) sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
+            float gs[WG][4];
+            double al = a.step0;
+#pragma unroll
+            for (int m = 0; m < WC; ++m) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float tw, g;
+                penalty_t<PM>(trial(r[e], (float)al, ud[e]), w[e], a, tw, g);
+                cst[m] += tw;
+#pragma unroll
+                for (int mm = 0; mm < WG; ++mm)
+                  if (m == wlo + mm) gs[mm][e] = g;
+              }
+              al *= a.shrink;
+            }
+#pragma unroll
+            for (int mm = 0; mm < WG; ++mm) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pk[mm * (K + 1) + K] += gs[mm][e] * gs[mm][e];
+#pragma unroll
+              for (int j = 0; j < K; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) pk[mm * (K + 1) + j] += u[4 * j + e] * gs[mm][e];
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < WC; ++m) rstage((double)cst[m], wred, m, NV);
+          stage_floats<WG * (K + 1)>(pk, wred, NV, WC);
+          team_sum(ra, team, rank, wred, NV, red, epoch, sprof);
+          LOGIC(after_iter<K>(cs, a, s, tid, red, wlo));
+        }
+        __syncthreads();
+        // apply an accepted step to the residual kept in shared memory
+        const float pa = (float)cs->pend_alpha;
+        if (pa != 0.f) {
+          for (int slot = 0; slot < nslots; ++slot) {
+            const int qi = slot * TM_NT + tid;
+            if (qi >= qcount) continue;
+            float r[4], ud[4];
+            f4(sR[qi], r);
+            f4(sD[qi], ud);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) r[e] = trial(r[e], pa, ud[e]);
+            sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
+          }
+        }
+        __syncthreads();
+        if (tid == 0) cs->pend_alpha = 0.0;
+        __syncthreads();
+      }
+    }
+
+    if (cs->status == ST_OK) {
+      // ---- geodesic step + relabel (manifold.py:116-197, tracker.py:146-147) ---
+      // With a re-orthonormalization due (every 1000th step) U' is written back
+      // unlabeled; the streamed k_gram / k_geo<QR> kernels that follow every
+      // launch apply U' R^-1 and relabel (manifold.py:192-196).
+      const bool geo = cs->do_geo != 0, qr = geo && cs->qr_now != 0;
+      const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s, ln = (float)cs->geo_ln;
+      float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
+      // epilogue of one row group with its final basis values u
+      auto finish_group = [&](int qi, const float* u) {
+        if (qi >= qcount) return;
+        const int pix = (q0 + qi) * 4;
+        const size_t off = (size_t)s * a.np + pix;
+        if (geo) {
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            if (j < k)
+              __stcs(reinterpret_cast<float4*>(Ug + (size_t)j * a.np + pix),
+                     make_float4(u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]));
+        }
+        if (qr) return;
+        float xh[4], bgn[4], rr[4];
+        f4(sX[qi], xh);
+        uint32_t nl = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float acc = 0.f;
+#pragma unroll
+          for (int j = 0; j < K; ++j) acc += u[4 * j + e] * (float)cs->y[j];
+          bgn[e] = acc;
+          rr[e] = __fsub_rn(xh[e], acc);
+          if (pix + e < a.P && fabs((double)rr[e]) >= a.delta) nl |= 1u << (8 * e);
+        }
+        *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
+        if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
+        if (a.res_out)
+          *reinterpret_cast<float4*>(static_cast<float*>(a.res_out) + off) = make_float4(rr[0], rr[1], rr[2], rr[3]);
+        if (a.bg_out) {
+          const float sc = (float)cs->std_cur;
+          float m4[4], b[4];
+          f4(sM[qi], m4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
+          *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + off) = make_float4(b[0], b[1], b[2], b[3]);
+        }
+      };
+
+      for (int slot = 0; slot < nslots; ++slot) {
+        const int qi = slot * TM_NT + tid;
+        float u[QC];
+        load_u(slot, u);
+        if (geo) {
+          float r[4], w[4];
+          f4(qi < qcount ? sR[qi] : make_float4(0.f, 0.f, 0.f, 0.f), r);
+          weights(qi, w);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float tw, g;
+            penalty_t<PM>(r[e], w[e], a, tw, g);
+            const float eta = -g;  // cost.py:103-112
+            float uv = 0.f, ug = 0.f;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              uv += u[4 * j + e] * (float)cs->v[j];
+              ug += u[4 * j + e] * (float)cs->grad[j];
+            }
+            const float coef = ga * uv - gsn * ((eta - ug) / ln);
+#pragma unroll
+            for (int j = 0; j < K; ++j) u[4 * j + e] += coef * (float)cs->v[j];
+          }
+        }
+        finish_group(qi, u);
+      }
+    }
+
+    // ---- commit the control block (one writer per stream) ------------------
+    __syncthreads();
+    if (rank == 0 && tid < (int)(sizeof(Ctl) / 8))
+      reinterpret_cast<double*>(a.ctl + s)[tid] = reinterpret_cast<const double*>(cs)[tid];
+    __syncthreads();
+  }
+#undef LOGIC
+  if (ra.prof && tid == 0) {
+    sprof[PROF_TOTAL] = gtimer() - t_start;
+    for (int i = 0; i < 8; ++i) ra.prof[(size_t)blockIdx.x * 8 + i] = sprof[i];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tbase));
+}
+
+}  // namespace prost

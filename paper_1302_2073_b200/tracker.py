@@ -347,7 +347,7 @@ _CORE_CACHE: dict = {}
 def _core_handle(m: int, params: ProstParams, precision: str, device: int) -> NativeTracker:
     # the kernel-path switches are read at handle creation: key on them too
     key = (m, params, precision, device, os.environ.get("PROST_RESIDENT"),
-           os.environ.get("PROST_NO_RESIDENT"))
+           os.environ.get("PROST_NO_RESIDENT"), os.environ.get("PROST_KERNEL"))
     h = _CORE_CACHE.get(key)
     if h is None:
         if len(_CORE_CACHE) > 8:

@@ -110,12 +110,13 @@ def test_fit_cases(precision):
             assert [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z[key + "counts"])
 
 
-@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32-resident"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32-resident", "fp32-streamed"])
 def test_periodic_reorthonormalization(precision, monkeypatch):
     """The unconditional QR at the 1000th geodesic step (manifold.py:192-196),
-    replayed from the reference's state at step 997."""
-    if precision == "fp32-resident":
-        monkeypatch.setenv("PROST_RESIDENT", "1")
+    replayed from the reference's state at step 997 (fp32: default TMEM kernel,
+    register-resident kernel, streamed kernels)."""
+    if precision.startswith("fp32-"):
+        monkeypatch.setenv("PROST_KERNEL", precision.split("-")[1])
         precision = "fp32"
     z = load("qr_chain")
     params = pkg.ProstParams(k=3, cfg=pkg.LpConfig(p=0.5, mu=0.06125), delta=0.35, omega=5e-5,
@@ -316,9 +317,11 @@ def test_large_batch_properties():
         assert np.linalg.norm(U.T @ U - np.eye(15)) < 1e-4
 
 
-def test_resident_kernel_matches_streamed(monkeypatch):
-    """The register-resident frame kernel (PROST_RESIDENT=1) and the
-    multi-kernel streamed path agree on a C3-shaped batch."""
+@pytest.mark.parametrize("mode", ["tmem", "resident"])
+def test_resident_kernels_match_streamed(mode, monkeypatch):
+    """The TMEM-resident (default for fp32 single-channel streams) and the
+    register-resident frame kernels agree with the multi-kernel streamed path
+    on a C3-shaped batch."""
     import torch
     from paper_1302_2073_b200 import _native as nat
 
@@ -327,22 +330,19 @@ def test_resident_kernel_matches_streamed(monkeypatch):
                         target_height=H, grayscale=True, i_init=4, seed=0)
     data = [c0_stream(F, W, H, seed=s) for s in range(S)]
     out = {}
-    for mode in ("resident", "streamed"):
-        if mode == "resident":
-            monkeypatch.setenv("PROST_RESIDENT", "1")
-        else:
-            monkeypatch.delenv("PROST_RESIDENT", raising=False)
+    for path, code in ((mode, {"tmem": 2, "resident": 1}[mode]), ("streamed", 0)):
+        monkeypatch.setenv("PROST_KERNEL", path)
         bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
-        assert bt.native.query(nat.Q_RESIDENT) == (1 if mode == "resident" else 0)
+        assert bt.native.query(nat.Q_RESIDENT) == code
         mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
         bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
         for f in range(F):
             fr = torch.from_numpy(np.stack([d[f] for d in data]).astype(np.float32)).cuda()
             info = bt.push(fr, background=bg, mask=mask, fit=True)
-        out[mode] = (mask.cpu().numpy(), bg.cpu().numpy(),
+        out[path] = (mask.cpu().numpy(), bg.cpu().numpy(),
                      [bt.native.get_core_state(s)[0] for s in range(S)],
                      [info[s].fit_cost for s in range(S)])
-    (m1, b1, U1, c1), (m2, b2, U2, c2) = out["resident"], out["streamed"]
+    (m1, b1, U1, c1), (m2, b2, U2, c2) = out[mode], out["streamed"]
     assert np.mean(m1 != m2) <= 0.001
     assert np.linalg.norm(b1 - b2) <= 1e-5 * np.linalg.norm(b2)
     for s in range(S):
