@@ -20,6 +20,9 @@ OUT = PKG / "_lib" / "libprost_b200.so"
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared", f"-I{ROOT / 'include'}",
+    # fp32 denormals flushed: every penalty input is >= mu > 0, and rsqrtf then
+    # maps to a single MUFU.RSQ (the fp64 parity instantiation is unaffected)
+    "-ftz=true",
 ]
 
 

@@ -155,6 +155,10 @@ Args make_args(prost_handle* h, int s0) {
   a.step0 = h->prm.initial_step;
   a.shrink = h->prm.shrink;
   a.c_armijo = h->prm.sufficient_decrease;
+  a.pf = (float)a.p;
+  a.half_pf = (float)a.half_p;
+  a.muf = (float)a.mu;
+  a.omegaf = (float)a.omega;
   return a;
 }
 

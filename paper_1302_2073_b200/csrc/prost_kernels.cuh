@@ -102,6 +102,7 @@ struct Args {
   int chunks, nvmax;
   int pipeline, max_iters, max_bt, i_init, pmode, n_real;
   double p, half_p, mu, delta, omega, t_init, t_min, tau, grad_tol, step0, shrink, c_armijo;
+  float pf, half_pf, muf, omegaf;  // fp32 copies for the per-element math
 };
 
 // ---------------------------------------------------------------------------
@@ -191,24 +192,24 @@ constexpr int PM_ANY = -1;
 
 template <int PM>
 __device__ __forceinline__ void penalty_t(float r, float w, const Args& a, float& tw, float& g) {
-  const float b = fmaf(r, r, (float)a.mu);
+  const float b = fmaf(r, r, a.muf);
   const int pm = PM == PM_ANY ? a.pmode : PM;
   if (pm == PM_HALF) {  // b^(1/4) and b^(-3/4) from two MUFU.RSQ
     const float h = rsqrtf(b);
     const float e = rsqrtf(h);
     tw = e * w;
-    g = (float)a.p * r * tw * (h * h);
+    g = 0.5f * r * tw * (h * h);
   } else if (pm == PM_ONE) {
     const float h = rsqrtf(b);
     tw = b * h * w;
-    g = (float)a.p * r * w * h;
+    g = r * w * h;
   } else if (pm == PM_TWO) {
     tw = b * w;
-    g = (float)a.p * r * w;
+    g = 2.f * r * w;
   } else {
     const float L = __log2f(b);
-    tw = exp2f((float)a.half_p * L) * w;
-    g = (float)a.p * r * tw * __frcp_rn(b);
+    tw = exp2f(a.half_pf * L) * w;
+    g = a.pf * r * tw * __frcp_rn(b);
   }
 }
 

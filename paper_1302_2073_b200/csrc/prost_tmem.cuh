@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ unsigned s_tbase;
   __shared__ unsigned long long sprof[8];
+  __shared__ float sfv[4][K];  // fp32 copies of y, d, v, grad for the per-element math
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -81,10 +82,23 @@ __global__ void __launch_bounds__(TM_NT, 1)
   const unsigned tbase = s_tbase + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 128);
   unsigned epoch = 0;
 
+#define SYNC_FLOATS()                      \
+  do {                                     \
+    if (tid < K) {                         \
+      sfv[0][tid] = (float)cs->y[tid];     \
+      sfv[1][tid] = (float)cs->d[tid];     \
+      sfv[2][tid] = (float)cs->v[tid];     \
+      sfv[3][tid] = (float)cs->grad[tid];  \
+    }                                      \
+  } while (0)
 #define LOGIC(call)                                                        \
   do {                                                                     \
     const unsigned long long tl0 = (ra.prof && tid == 0) ? gtimer() : 0;   \
-    if (tid < 32) call;                                                    \
+    if (tid < 32) {                                                        \
+      call;                                                                \
+      __syncwarp();                                                        \
+      SYNC_FLOATS();                                                       \
+    }                                                                      \
     if (ra.prof && tid == 0) sprof[PROF_LOGIC] += gtimer() - tl0;          \
   } while (0)
 
@@ -144,10 +158,11 @@ __global__ void __launch_bounds__(TM_NT, 1)
         reinterpret_cast<double*>(cs)[tid] = __ldcg(reinterpret_cast<const double*>(a.ctl + s) + tid);
       __syncthreads();
       if (tid == 0) cs->no_info = rank != 0;
+      SYNC_FLOATS();
       __syncthreads();
       if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += gtimer() - tw0;
     }
-    const float omega = (float)a.omega;
+    const float omega = a.omegaf;
     auto weights = [&](int qi, float* w) {
       const uint32_t lb = qi < qcount ? sL[qi] : 0u;
       const int pix = (q0 + qi) * 4;
@@ -260,6 +275,8 @@ __global__ void __launch_bounds__(TM_NT, 1)
         if (tid < 32) {
           if (red[K] > 0.0) mark_nonfinite(cs, a, s, tid);
           else if (tid < k) cs->y[tid] = red[tid];
+          __syncwarp();
+          SYNC_FLOATS();
         }
         __syncthreads();
       }
@@ -283,7 +300,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
           for (int e = 0; e < 4; ++e) {
             float uy = 0.f;
 #pragma unroll
-            for (int j = 0; j < K; ++j) uy += u[4 * j + e] * (float)cs->y[j];
+            for (int j = 0; j < K; ++j) uy += u[4 * j + e] * sfv[0][j];
             r[e] = __fsub_rn(xh[e], uy);
             float tw;
             penalty_t<PM>(r[e], w[e], a, tw, g[e]);
@@ -384,7 +401,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
             for (int e = 0; e < 4; ++e) ud[e] = 0.f;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-              const float dj = (float)cs->d[j];
+              const float dj = sfv[1][j];
 #pragma unroll
               for (int e = 0; e < 4; ++e) ud[e] += u[4 * j + e] * dj;
             }
@@ -469,7 +486,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         for (int e = 0; e < 4; ++e) {
           float acc = 0.f;
 #pragma unroll
-          for (int j = 0; j < K; ++j) acc += u[4 * j + e] * (float)cs->y[j];
+          for (int j = 0; j < K; ++j) acc += u[4 * j + e] * sfv[0][j];
           bgn[e] = acc;
           rr[e] = __fsub_rn(xh[e], acc);
           if (pix + e < a.P && fabs((double)rr[e]) >= a.delta) nl |= 1u << (8 * e);
@@ -505,12 +522,12 @@ __global__ void __launch_bounds__(TM_NT, 1)
             float uv = 0.f, ug = 0.f;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-              uv += u[4 * j + e] * (float)cs->v[j];
-              ug += u[4 * j + e] * (float)cs->grad[j];
+              uv += u[4 * j + e] * sfv[2][j];
+              ug += u[4 * j + e] * sfv[3][j];
             }
             const float coef = ga * uv - gsn * ((eta - ug) / ln);
 #pragma unroll
-            for (int j = 0; j < K; ++j) u[4 * j + e] += coef * (float)cs->v[j];
+            for (int j = 0; j < K; ++j) u[4 * j + e] += coef * sfv[2][j];
           }
         }
         finish_group(qi, u);
@@ -524,6 +541,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
     __syncthreads();
   }
 #undef LOGIC
+#undef SYNC_FLOATS
   if (ra.prof && tid == 0) {
     sprof[PROF_TOTAL] = gtimer() - t_start;
     for (int i = 0; i < 8; ++i) ra.prof[(size_t)blockIdx.x * 8 + i] = sprof[i];
