@@ -167,19 +167,24 @@ __device__ __forceinline__ void rstage(double x, double* wred, int slot, int nv)
 
 // 32 floats per lane -> lane L ends with the warp sum of value L (butterfly
 // reduce-scatter: 31 shuffles instead of 32 x 5).
-__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
+template <int OFF>
+__device__ __forceinline__ void rs_step(float (&v)[32], int lane) {
+  const bool up = (lane & OFF) != 0;
 #pragma unroll
-  for (int lg = 4; lg >= 0; --lg) {
-    const int off = 1 << lg;
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < off; ++i) {
-      const float keep = up ? v[i + off] : v[i];
-      const float send = up ? v[i] : v[i + off];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
+  for (int i = 0; i < OFF; ++i) {
+    const float keep = up ? v[i + OFF] : v[i];
+    const float send = up ? v[i] : v[i + OFF];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
   }
+}
+__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
+  // compile-time offsets keep v[] in registers
+  const int lane = threadIdx.x & 31;
+  rs_step<16>(v, lane);
+  rs_step<8>(v, lane);
+  rs_step<4>(v, lane);
+  rs_step<2>(v, lane);
+  rs_step<1>(v, lane);
   return v[0];
 }
 

@@ -5,12 +5,13 @@
 // reductions are team-wide sums through double-buffered global slots and a
 // release/acquire counter barrier, after which every CTA runs the scalar
 // logic itself).  The difference is where a CTA keeps its slice of U: each
-// thread owns QT row groups (4 rows x k columns each) in its lane of tensor
-// memory (tcgen05.st once per frame, tcgen05.ld in every phase) plus, when the
-// slice is larger, one more group in shared memory.  With 256 KB of TMEM +
-// shared memory per SM a C3 stream (76,800 x 15 fp32 = 4.6 MB) fits on 14
-// SMs, so ~10 streams are in flight at once — enough to cover the latency of
-// the reduction chain — and U still crosses HBM exactly once each way.
+// thread owns QT row groups (4 rows x k values) in its lane of tensor memory
+// (written once per frame with tcgen05.st, read row by row with tcgen05.ld in
+// every phase), plus, when the slice is larger, row groups in shared memory.
+// With 256 KB of TMEM + shared memory per SM a C3 stream (76,800 x 15 fp32 =
+// 4.6 MB) fits on 13 SMs, so 11 streams are in flight at once, and U crosses
+// HBM exactly once each way per frame.  Working one row (k values) at a time
+// keeps the live basis registers at 16 instead of 4k.
 #pragma once
 
 #include "prost_resident.cuh"
@@ -22,27 +23,43 @@ constexpr int TM_NT = 512;  // threads per CTA: 16 warps = 4 per TMEM lane quart
 
 template <int K>
 struct TmemGeom {
-  static constexpr int QCOLS = 4 * K;  // TMEM columns per row group
-  // column stride between a thread's row groups: a power of two, so every
-  // tcgen05 access (x32/x16/x8/x4) starts at a column aligned to its width
-  static constexpr int STRIDE = QCOLS <= 16 ? 16 : (QCOLS <= 32 ? 32 : 64);
-  static constexpr int QT = 128 / STRIDE;  // row groups per thread in TMEM
+  // columns per row (power of two >= k: every tcgen05 access is width-aligned)
+  static constexpr int RS = K <= 4 ? 4 : (K <= 8 ? 8 : 16);
+  static constexpr int QW = 4 * RS;        // columns per row group
+  static constexpr int QT = 128 / QW;      // row groups per thread in TMEM
 };
 
 // Dynamic shared memory of k_tmem<K> for qpc row groups per CTA.
 template <int K>
 __host__ __device__ constexpr size_t tmem_smem(int qpc) {
   const int qs = qpc > TmemGeom<K>::QT * TM_NT ? qpc - TmemGeom<K>::QT * TM_NT : 0;
-  return (size_t)K * qs * 16                    // basis row groups kept in shared memory
+  return (size_t)4 * K * qs * 4                 // basis row groups kept in shared memory
          + (size_t)qpc * (4 * 16 + 4)           // r, u_dir, normalized frame, mean, labels
          + (size_t)(TM_NT / 32 + 1) * RES_RNV_MAX * 8 + sizeof(Ctl) + 64;
+}
+
+template <int RS>
+__device__ __forceinline__ void tmem_ld_row(unsigned taddr, float (&v)[RS]) {
+  if constexpr (RS == 16) tmem_ld16(taddr, v);
+  else if constexpr (RS == 8) tmem_ld8(taddr, v);
+  else tmem_ld4(taddr, v);
+}
+template <int RS>
+__device__ __forceinline__ void tmem_st_row(unsigned taddr, const float (&v)[RS]) {
+  if constexpr (RS == 16) tmem_st16(taddr, v);
+  else if constexpr (RS == 8) tmem_st8(taddr, v);
+  else tmem_st4(taddr, v);
+}
+
+__device__ __forceinline__ void f4(float4 v, float (&o)[4]) {
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 }
 
 template <int K, int PM>
 __global__ void __launch_bounds__(TM_NT, 1)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
-  constexpr int QC = Geo::QCOLS, QT = Geo::QT, QS = Geo::STRIDE;
+  constexpr int RS = Geo::RS, QW = Geo::QW, QT = Geo::QT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ unsigned s_tbase;
   __shared__ unsigned long long sprof[8];
@@ -57,12 +74,12 @@ __global__ void __launch_bounds__(TM_NT, 1)
   const int nslots = (qcount + TM_NT - 1) / TM_NT;  // uniform across the CTA
   const int qs = qpc > QT * TM_NT ? qpc - QT * TM_NT : 0;
 
-  float4* sU = reinterpret_cast<float4*>(smem_raw);  // [K][qs]
-  float4* sR = sU + (size_t)K * qs;                  // [qpc] residual
-  float4* sD = sR + qpc;                             // [qpc] u_dir
-  float4* sX = sD + qpc;                             // [qpc] normalized frame
-  float4* sM = sX + qpc;                             // [qpc] running mean
-  uint32_t* sL = reinterpret_cast<uint32_t*>(sM + qpc);  // [qpc] label bytes
+  float* sU = reinterpret_cast<float*>(smem_raw);    // [4][K][qs] row-major per row group
+  float4* sR = reinterpret_cast<float4*>(sU + 4 * K * qs);  // [qpc] residual
+  float4* sD = sR + qpc;                                    // [qpc] u_dir
+  float4* sX = sD + qpc;                                    // [qpc] normalized frame
+  float4* sM = sX + qpc;                                    // [qpc] running mean
+  uint32_t* sL = reinterpret_cast<uint32_t*>(sM + qpc);     // [qpc] label bytes
   double* wred = reinterpret_cast<double*>(sL + ((qpc + 1) / 2) * 2);
   double* red = wred + (size_t)(TM_NT / 32) * RES_RNV_MAX;
   Ctl* cs = reinterpret_cast<Ctl*>(red + RES_RNV_MAX);
@@ -79,7 +96,8 @@ __global__ void __launch_bounds__(TM_NT, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   // this thread's lane and columns: lane quarter = warp % 4, column block = warp / 4
-  const unsigned tbase = s_tbase + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 128);
+  const unsigned tbase =
+      s_tbase + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 128);
   unsigned epoch = 0;
 
 #define SYNC_FLOATS()                      \
@@ -102,31 +120,28 @@ __global__ void __launch_bounds__(TM_NT, 1)
     if (ra.prof && tid == 0) sprof[PROF_LOGIC] += gtimer() - tl0;          \
   } while (0)
 
-  // row group (slot) -> basis registers
-  auto load_u = [&](int slot, float* u) {
+  // One row (e) of row group `slot`: the k basis values of that coordinate.
+  // TMEM rows are read by the whole warp (tcgen05 is warp-collective).
+  auto load_row = [&](int slot, int e, float (&u)[RS]) {
     if (slot < QT) {
-      tmem_ld<QC>(tbase + slot * QS, u);
+      tmem_ld_row<RS>(tbase + slot * QW + e * RS, u);
       tmem_wait_ld();
     } else {
       const int i = slot * TM_NT + tid - QT * TM_NT;
       const bool ok = slot * TM_NT + tid < qcount;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const float4 t = ok ? sU[(size_t)j * qs + i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        u[4 * j + 0] = t.x; u[4 * j + 1] = t.y; u[4 * j + 2] = t.z; u[4 * j + 3] = t.w;
-      }
+      for (int j = 0; j < RS; ++j) u[j] = (ok && j < K) ? sU[(e * K + j) * qs + i] : 0.f;
     }
   };
-  auto store_u_onchip = [&](int slot, const float* u) {
-    if (slot < QT) {
-      tmem_st<QC>(tbase + slot * QS, u);
-    } else if (slot * TM_NT + tid < qcount) {
-      const int i = slot * TM_NT + tid - QT * TM_NT;
+  const float omega = a.omegaf;
+  auto weights = [&](int qi, float (&w)[4]) {
+    const uint32_t lb = qi < qcount ? sL[qi] : 0u;
+    const int pix = (q0 + qi) * 4;
 #pragma unroll
-      for (int j = 0; j < K; ++j) sU[(size_t)j * qs + i] = make_float4(u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
-    }
+    for (int e = 0; e < 4; ++e)
+      w[e] = (qi < qcount && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
   };
-  auto f4 = [](float4 v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; };
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
 
   for (int s = team; s < ra.S; s += T) {
     if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
@@ -138,19 +153,30 @@ __global__ void __launch_bounds__(TM_NT, 1)
         const int qi = slot * TM_NT + tid;  // row group within the slice
         const bool ok = qi < qcount;
         const size_t off = (size_t)(q0 + qi) * 4;
-        float u[QC];
+        float4 p[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ok && j < k) t = __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + off));
-          u[4 * j] = t.x; u[4 * j + 1] = t.y; u[4 * j + 2] = t.z; u[4 * j + 3] = t.w;
-        }
-        store_u_onchip(slot, u);
+        for (int j = 0; j < K; ++j)
+          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + off)) : z4;
         if (ok) {
           sX[qi] = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + (size_t)s * a.np + off));
-          sM[qi] = a.pipeline ? *reinterpret_cast<const float4*>(static_cast<const float*>(a.mean) + (size_t)s * a.np + off)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          sM[qi] = a.pipeline ? *reinterpret_cast<const float4*>(static_cast<const float*>(a.mean) + (size_t)s * a.np + off) : z4;
           sL[qi] = *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + (q0 + qi) * 4);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float row[RS];
+#pragma unroll
+          for (int j = 0; j < RS; ++j) {
+            const float4 t = j < K ? p[j] : z4;
+            row[j] = e == 0 ? t.x : (e == 1 ? t.y : (e == 2 ? t.z : t.w));
+          }
+          if (slot < QT) {
+            tmem_st_row<RS>(tbase + slot * QW + e * RS, row);
+          } else if (ok) {
+            const int i = qi - QT * TM_NT;
+#pragma unroll
+            for (int j = 0; j < K; ++j) sU[(e * K + j) * qs + i] = row[j];
+          }
         }
       }
       tmem_wait_st();
@@ -162,14 +188,6 @@ __global__ void __launch_bounds__(TM_NT, 1)
       __syncthreads();
       if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += gtimer() - tw0;
     }
-    const float omega = a.omegaf;
-    auto weights = [&](int qi, float* w) {
-      const uint32_t lb = qi < qcount ? sL[qi] : 0u;
-      const int pix = (q0 + qi) * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        w[e] = (qi < qcount && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
-    };
 
     // ---- frame start: running statistics (pipeline.py:120-140) -------------
     const bool upd = a.pipeline && !cs->frozen && cs->frame_index < a.i_init;
@@ -261,13 +279,15 @@ __global__ void __launch_bounds__(TM_NT, 1)
         for (int j = 0; j < K; ++j) pk[j] = 0.f;
         for (int slot = 0; slot < nslots; ++slot) {
           const int qi = slot * TM_NT + tid;
-          float u[QC], xh[4];
-          load_u(slot, u);
-          f4(qi < qcount ? sX[qi] : make_float4(0.f, 0.f, 0.f, 0.f), xh);
+          float xh[4];
+          f4(qi < qcount ? sX[qi] : z4, xh);
 #pragma unroll
-          for (int j = 0; j < K; ++j)
+          for (int e = 0; e < 4; ++e) {
+            float u[RS];
+            load_row(slot, e, u);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) pk[j] += u[4 * j + e] * xh[e];
+            for (int j = 0; j < K; ++j) pk[j] += u[j] * xh[e];
+          }
         }
         stage_floats<K>(pk, wred, K + 1, 0);
         rstage(bad ? 1.0 : 0.0, wred, K, K + 1);
@@ -291,27 +311,26 @@ __global__ void __launch_bounds__(TM_NT, 1)
         for (int j = 0; j <= K; ++j) pk[j] = 0.f;
         for (int slot = 0; slot < nslots; ++slot) {
           const int qi = slot * TM_NT + tid;
-          float u[QC], xh[4], w[4], r[4], g[4];
-          load_u(slot, u);
-          f4(qi < qcount ? sX[qi] : make_float4(0.f, 0.f, 0.f, 0.f), xh);
+          float xh[4], w[4], r[4];
+          f4(qi < qcount ? sX[qi] : z4, xh);
           weights(qi, w);
           float tc = 0.f;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
+            float u[RS];
+            load_row(slot, e, u);
             float uy = 0.f;
 #pragma unroll
-            for (int j = 0; j < K; ++j) uy += u[4 * j + e] * sfv[0][j];
+            for (int j = 0; j < K; ++j) uy += u[j] * sfv[0][j];
             r[e] = __fsub_rn(xh[e], uy);
-            float tw;
-            penalty_t<PM>(r[e], w[e], a, tw, g[e]);
+            float tw, g;
+            penalty_t<PM>(r[e], w[e], a, tw, g);
             tc += tw;
-            pk[K] += g[e] * g[e];
+            pk[K] += g * g;
+#pragma unroll
+            for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
           }
           cost += (double)tc;
-#pragma unroll
-          for (int j = 0; j < K; ++j)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) pk[j] += u[4 * j + e] * g[e];
           if (qi < qcount) sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
         }
         rstage(cost, wred, 0, K + 3);
@@ -363,21 +382,20 @@ __global__ void __launch_bounds__(TM_NT, 1)
           for (int j = 0; j <= K; ++j) pk[j] = 0.f;
           for (int slot = 0; slot < nslots; ++slot) {
             const int qi = slot * TM_NT + tid;
-            float u[QC], r[4], ud[4], w[4], g[4];
-            load_u(slot, u);
-            f4(qi < qcount ? sR[qi] : make_float4(0.f, 0.f, 0.f, 0.f), r);
-            f4(qi < qcount ? sD[qi] : make_float4(0.f, 0.f, 0.f, 0.f), ud);
+            float r[4], ud[4], w[4];
+            f4(qi < qcount ? sR[qi] : z4, r);
+            f4(qi < qcount ? sD[qi] : z4, ud);
             weights(qi, w);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              float tw;
-              penalty_t<PM>(trial(r[e], al, ud[e]), w[e], a, tw, g[e]);
-              pk[K] += g[e] * g[e];
+              float u[RS];
+              load_row(slot, e, u);
+              float tw, g;
+              penalty_t<PM>(trial(r[e], al, ud[e]), w[e], a, tw, g);
+              pk[K] += g * g;
+#pragma unroll
+              for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
             }
-#pragma unroll
-            for (int j = 0; j < K; ++j)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) pk[j] += u[4 * j + e] * g[e];
           }
           stage_floats<K + 1>(pk, wred, K + 1, 0);
           team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
@@ -385,6 +403,15 @@ __global__ void __launch_bounds__(TM_NT, 1)
         } else {
           constexpr int NV = WC + WG * (K + 1);
           const int wlo = cs->gwin_lo;
+          float al[WC];
+          {
+            double v = a.step0;
+#pragma unroll
+            for (int m = 0; m < WC; ++m) {
+              al[m] = (float)v;
+              v *= a.shrink;
+            }
+          }
           float cst[WC];
           float pk[WG * (K + 1)];
 #pragma unroll
@@ -393,43 +420,36 @@ __global__ void __launch_bounds__(TM_NT, 1)
           for (int i = 0; i < WG * (K + 1); ++i) pk[i] = 0.f;
           for (int slot = 0; slot < nslots; ++slot) {
             const int qi = slot * TM_NT + tid;
-            float u[QC], r[4], ud[4], w[4];
-            load_u(slot, u);
-            f4(qi < qcount ? sR[qi] : make_float4(0.f, 0.f, 0.f, 0.f), r);
+            float r[4], w[4], ud[4];
+            f4(qi < qcount ? sR[qi] : z4, r);
             weights(qi, w);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) ud[e] = 0.f;
+            for (int e = 0; e < 4; ++e) {
+              float u[RS];
+              load_row(slot, e, u);
+              float d = 0.f;
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-              const float dj = sfv[1][j];
+              for (int j = 0; j < K; ++j) d += u[j] * sfv[1][j];
+              ud[e] = d;
+              float gs[WG];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) ud[e] += u[4 * j + e] * dj;
-            }
-            if (qi < qcount) sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
-            float gs[WG][4];
-            double al = a.step0;
+              for (int mm = 0; mm < WG; ++mm) gs[mm] = 0.f;
 #pragma unroll
-            for (int m = 0; m < WC; ++m) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
+              for (int m = 0; m < WC; ++m) {
                 float tw, g;
-                penalty_t<PM>(trial(r[e], (float)al, ud[e]), w[e], a, tw, g);
+                penalty_t<PM>(trial(r[e], al[m], d), w[e], a, tw, g);
                 cst[m] += tw;
 #pragma unroll
-                for (int mm = 0; mm < WG; ++mm)
-                  if (m == wlo + mm) gs[mm][e] = g;
+                for (int mm = 0; mm < WG; ++mm) gs[mm] = (m == wlo + mm) ? g : gs[mm];
               }
-              al *= a.shrink;
+#pragma unroll
+              for (int mm = 0; mm < WG; ++mm) {
+                pk[mm * (K + 1) + K] += gs[mm] * gs[mm];
+#pragma unroll
+                for (int j = 0; j < K; ++j) pk[mm * (K + 1) + j] += u[j] * gs[mm];
+              }
             }
-#pragma unroll
-            for (int mm = 0; mm < WG; ++mm) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) pk[mm * (K + 1) + K] += gs[mm][e] * gs[mm][e];
-#pragma unroll
-              for (int j = 0; j < K; ++j)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) pk[mm * (K + 1) + j] += u[4 * j + e] * gs[mm][e];
-            }
+            if (qi < qcount) sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
           }
 #pragma unroll
           for (int m = 0; m < WC; ++m) rstage((double)cst[m], wred, m, NV);
@@ -466,19 +486,44 @@ __global__ void __launch_bounds__(TM_NT, 1)
       const bool geo = cs->do_geo != 0, qr = geo && cs->qr_now != 0;
       const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s, ln = (float)cs->geo_ln;
       float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
-      // epilogue of one row group with its final basis values u
-      auto finish_group = [&](int qi, const float* u) {
-        if (qi >= qcount) return;
+      for (int slot = 0; slot < nslots; ++slot) {
+        const int qi = slot * TM_NT + tid;
+        const bool ok = qi < qcount;
         const int pix = (q0 + qi) * 4;
-        const size_t off = (size_t)s * a.np + pix;
+        float r[4], w[4];
+        f4(ok ? sR[qi] : z4, r);
+        weights(qi, w);
+        float up[4][K];  // U' rows of this row group
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float u[RS];
+          load_row(slot, e, u);
+          float coef = 0.f;
+          if (geo) {
+            float tw, g;
+            penalty_t<PM>(r[e], w[e], a, tw, g);
+            const float eta = -g;  // cost.py:103-112
+            float uv = 0.f, ug = 0.f;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+              uv += u[j] * sfv[2][j];
+              ug += u[j] * sfv[3][j];
+            }
+            coef = ga * uv - gsn * ((eta - ug) / ln);
+          }
+#pragma unroll
+          for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
+        }
+        if (!ok) continue;
         if (geo) {
 #pragma unroll
           for (int j = 0; j < K; ++j)
             if (j < k)
               __stcs(reinterpret_cast<float4*>(Ug + (size_t)j * a.np + pix),
-                     make_float4(u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]));
+                     make_float4(up[0][j], up[1][j], up[2][j], up[3][j]));
         }
-        if (qr) return;
+        if (qr) continue;
+        const size_t off = (size_t)s * a.np + pix;
         float xh[4], bgn[4], rr[4];
         f4(sX[qi], xh);
         uint32_t nl = 0;
@@ -486,7 +531,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         for (int e = 0; e < 4; ++e) {
           float acc = 0.f;
 #pragma unroll
-          for (int j = 0; j < K; ++j) acc += u[4 * j + e] * sfv[0][j];
+          for (int j = 0; j < K; ++j) acc += up[e][j] * sfv[0][j];
           bgn[e] = acc;
           rr[e] = __fsub_rn(xh[e], acc);
           if (pix + e < a.P && fabs((double)rr[e]) >= a.delta) nl |= 1u << (8 * e);
@@ -504,33 +549,6 @@ __global__ void __launch_bounds__(TM_NT, 1)
             b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
           *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + off) = make_float4(b[0], b[1], b[2], b[3]);
         }
-      };
-
-      for (int slot = 0; slot < nslots; ++slot) {
-        const int qi = slot * TM_NT + tid;
-        float u[QC];
-        load_u(slot, u);
-        if (geo) {
-          float r[4], w[4];
-          f4(qi < qcount ? sR[qi] : make_float4(0.f, 0.f, 0.f, 0.f), r);
-          weights(qi, w);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float tw, g;
-            penalty_t<PM>(r[e], w[e], a, tw, g);
-            const float eta = -g;  // cost.py:103-112
-            float uv = 0.f, ug = 0.f;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-              uv += u[4 * j + e] * sfv[2][j];
-              ug += u[4 * j + e] * sfv[3][j];
-            }
-            const float coef = ga * uv - gsn * ((eta - ug) / ln);
-#pragma unroll
-            for (int j = 0; j < K; ++j) u[4 * j + e] += coef * sfv[2][j];
-          }
-        }
-        finish_group(qi, u);
       }
     }
 
