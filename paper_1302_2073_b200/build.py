@@ -13,8 +13,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SRC = PKG / "csrc" / "prost_b200.cu"
-DEPS = [SRC, PKG / "csrc" / "prost_kernels.cuh", PKG / "csrc" / "prost_phases.cuh",
-        ROOT / "include" / "prost_b200.h"]
+DEPS = sorted((PKG / "csrc").glob("*.cu*")) + sorted((ROOT / "include").glob("*.h")) + [
+    Path(__file__).resolve()]
 OUT = PKG / "_lib" / "libprost_b200.so"
 
 NVCC_FLAGS = [
