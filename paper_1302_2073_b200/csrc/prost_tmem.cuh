@@ -33,8 +33,8 @@ struct TmemGeom {
 template <int K>
 __host__ __device__ constexpr size_t tmem_smem(int qpc) {
   const int qs = qpc > TmemGeom<K>::QT * TM_NT ? qpc - TmemGeom<K>::QT * TM_NT : 0;
-  return (size_t)4 * K * qs * 4                 // basis row groups kept in shared memory
-         + (size_t)qpc * (4 * 16 + 4)           // r, u_dir, normalized frame, mean, labels
+  return (size_t)16 * TmemGeom<K>::RS * qs     // basis row groups kept in shared memory
+         + (size_t)qpc * (3 * 16 + 4)           // r, u_dir, normalized frame, labels
          + (size_t)(TM_NT / 32 + 1) * RES_RNV_MAX * 8 + sizeof(Ctl) + 64;
 }
 
@@ -74,12 +74,14 @@ __global__ void __launch_bounds__(TM_NT, 1)
   const int nslots = (qcount + TM_NT - 1) / TM_NT;  // uniform across the CTA
   const int qs = qpc > QT * TM_NT ? qpc - QT * TM_NT : 0;
 
-  float* sU = reinterpret_cast<float*>(smem_raw);    // [4][K][qs] row-major per row group
-  float4* sR = reinterpret_cast<float4*>(sU + 4 * K * qs);  // [qpc] residual
+  // basis rows kept in shared memory: [row e][4-column group][row group] float4,
+  // so a thread reads one row with RS/4 conflict-free 16-byte loads
+  float4* sU = reinterpret_cast<float4*>(smem_raw);         // [4][RS/4][qs]
+  float4* sR = sU + (size_t)RS * qs;                        // [qpc] residual
   float4* sD = sR + qpc;                                    // [qpc] u_dir
   float4* sX = sD + qpc;                                    // [qpc] normalized frame
-  float4* sM = sX + qpc;                                    // [qpc] running mean
-  uint32_t* sL = reinterpret_cast<uint32_t*>(sM + qpc);     // [qpc] label bytes
+  uint32_t* sL = reinterpret_cast<uint32_t*>(sX + qpc);     // [qpc] label bytes
+  const float* Mg = static_cast<const float*>(a.mean);      // running mean stays in global/L2
   double* wred = reinterpret_cast<double*>(sL + ((qpc + 1) / 2) * 2);
   double* red = wred + (size_t)(TM_NT / 32) * RES_RNV_MAX;
   Ctl* cs = reinterpret_cast<Ctl*>(red + RES_RNV_MAX);
@@ -129,8 +131,12 @@ __global__ void __launch_bounds__(TM_NT, 1)
     } else {
       const int i = slot * TM_NT + tid - QT * TM_NT;
       const bool ok = slot * TM_NT + tid < qcount;
+      const float4* rp = sU + (size_t)(e * (RS / 4)) * qs + i;
 #pragma unroll
-      for (int j = 0; j < RS; ++j) u[j] = (ok && j < K) ? sU[(e * K + j) * qs + i] : 0.f;
+      for (int g4 = 0; g4 < RS / 4; ++g4) {
+        const float4 t = ok ? rp[(size_t)g4 * qs] : make_float4(0.f, 0.f, 0.f, 0.f);
+        u[4 * g4] = t.x; u[4 * g4 + 1] = t.y; u[4 * g4 + 2] = t.z; u[4 * g4 + 3] = t.w;
+      }
     }
   };
   const float omega = a.omegaf;
@@ -159,7 +165,6 @@ __global__ void __launch_bounds__(TM_NT, 1)
           p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + off)) : z4;
         if (ok) {
           sX[qi] = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + (size_t)s * a.np + off));
-          sM[qi] = a.pipeline ? *reinterpret_cast<const float4*>(static_cast<const float*>(a.mean) + (size_t)s * a.np + off) : z4;
           sL[qi] = *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + (q0 + qi) * 4);
         }
 #pragma unroll
@@ -173,9 +178,10 @@ __global__ void __launch_bounds__(TM_NT, 1)
           if (slot < QT) {
             tmem_st_row<RS>(tbase + slot * QW + e * RS, row);
           } else if (ok) {
-            const int i = qi - QT * TM_NT;
+            float4* rp = sU + (size_t)(e * (RS / 4)) * qs + (qi - QT * TM_NT);
 #pragma unroll
-            for (int j = 0; j < K; ++j) sU[(e * K + j) * qs + i] = row[j];
+            for (int g4 = 0; g4 < RS / 4; ++g4)
+              rp[(size_t)g4 * qs] = make_float4(row[4 * g4], row[4 * g4 + 1], row[4 * g4 + 2], row[4 * g4 + 3]);
           }
         }
       }
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         const int pix = (q0 + qi) * 4;
         float xv[4], mv[4], xh[4];
         f4(sX[qi], xv);
-        f4(sM[qi], mv);
+        f4(a.pipeline ? *reinterpret_cast<const float4*>(Mg + (size_t)s * a.np + pix) : z4, mv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           bad |= !isfinite(xv[e]);
@@ -267,8 +273,8 @@ __global__ void __launch_bounds__(TM_NT, 1)
         }
         sX[qi] = make_float4(xh[0], xh[1], xh[2], xh[3]);
         if (upd) {
-          sM[qi] = make_float4(mv[0], mv[1], mv[2], mv[3]);
-          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + (size_t)s * a.np + pix) = sM[qi];
+          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + (size_t)s * a.np + pix) =
+              make_float4(mv[0], mv[1], mv[2], mv[3]);
         }
       }
 
@@ -431,17 +437,41 @@ __global__ void __launch_bounds__(TM_NT, 1)
 #pragma unroll
               for (int j = 0; j < K; ++j) d += u[j] * sfv[1][j];
               ud[e] = d;
-              float gs[WG];
+              // trial costs for every window step; the gradient only for the
+              // speculative pair (same arithmetic as penalty_t, split)
+              float ts[WG], hs[WG], es[WG];
 #pragma unroll
-              for (int mm = 0; mm < WG; ++mm) gs[mm] = 0.f;
+              for (int mm = 0; mm < WG; ++mm) ts[mm] = hs[mm] = es[mm] = 0.f;
 #pragma unroll
               for (int m = 0; m < WC; ++m) {
-                float tw, g;
-                penalty_t<PM>(trial(r[e], al[m], d), w[e], a, tw, g);
-                cst[m] += tw;
+                const float t = trial(r[e], al[m], d);
+                if (PM == PM_HALF) {
+                  const float b = fmaf(t, t, a.muf);
+                  const float h = rsqrtf(b);
+                  const float q = rsqrtf(h);
+                  cst[m] += q * w[e];
 #pragma unroll
-                for (int mm = 0; mm < WG; ++mm) gs[mm] = (m == wlo + mm) ? g : gs[mm];
+                  for (int mm = 0; mm < WG; ++mm) {
+                    const bool sel = m == wlo + mm;
+                    ts[mm] = sel ? t : ts[mm];
+                    hs[mm] = sel ? h : hs[mm];
+                    es[mm] = sel ? q : es[mm];
+                  }
+                } else {
+                  float tw, g;
+                  penalty_t<PM>(t, w[e], a, tw, g);
+                  cst[m] += tw;
+#pragma unroll
+                  for (int mm = 0; mm < WG; ++mm) {
+                    const bool sel = m == wlo + mm;
+                    ts[mm] = sel ? g : ts[mm];
+                  }
+                }
               }
+              float gs[WG];
+#pragma unroll
+              for (int mm = 0; mm < WG; ++mm)
+                gs[mm] = PM == PM_HALF ? 0.5f * ts[mm] * (es[mm] * w[e]) * (hs[mm] * hs[mm]) : ts[mm];
 #pragma unroll
               for (int mm = 0; mm < WG; ++mm) {
                 pk[mm * (K + 1) + K] += gs[mm] * gs[mm];
@@ -543,7 +573,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         if (a.bg_out) {
           const float sc = (float)cs->std_cur;
           float m4[4], b[4];
-          f4(sM[qi], m4);
+          f4(a.pipeline ? *reinterpret_cast<const float4*>(Mg + off) : z4, m4);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
