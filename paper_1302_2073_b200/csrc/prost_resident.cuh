@@ -31,6 +31,7 @@ struct RArgs {
   double* rpart;    // [2][T][rnv][G] reduction slots (value-major)
   int S;            // streams
   unsigned long long* prof;  // [gridDim][8] optional timing counters (ns), or null
+  int stagger_ns;            // start delay of odd teams (k_tmem), 0 = none
 };
 
 // Timing counters of one CTA (thread 0, %globaltimer ns): see PROF_* below.

@@ -55,6 +55,20 @@ __device__ __forceinline__ void f4(float4 v, float (&o)[4]) {
   o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
 }
 
+// k-term dot product with four independent partial sums (short FMA chains)
+template <int K>
+__device__ __forceinline__ float dotk(const float* u, const float* v) {
+  float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+  for (int j = 0; j < K; j += 4) {
+    p0 = fmaf(u[j], v[j], p0);
+    if (j + 1 < K) p1 = fmaf(u[j + 1], v[j + 1], p1);
+    if (j + 2 < K) p2 = fmaf(u[j + 2], v[j + 2], p2);
+    if (j + 3 < K) p3 = fmaf(u[j + 3], v[j + 3], p3);
+  }
+  return (p0 + p1) + (p2 + p3);
+}
+
 template <int K, int PM>
 __global__ void __launch_bounds__(TM_NT, 1)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
@@ -148,6 +162,14 @@ __global__ void __launch_bounds__(TM_NT, 1)
       w[e] = (qi < qcount && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
   };
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  // Stagger the teams: rounds are near-identical in length, so without an
+  // offset all teams load (and store) their slices at the same moment and the
+  // HBM traffic comes in bursts.  Odd teams start half a round late (ra.stagger_ns).
+  if ((team & 1) && ra.stagger_ns > 0) {
+    const unsigned long long t0 = gtimer();
+    while (gtimer() - t0 < (unsigned long long)ra.stagger_ns) __nanosleep(1000);
+  }
 
   for (int s = team; s < ra.S; s += T) {
     if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
@@ -325,9 +347,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
           for (int e = 0; e < 4; ++e) {
             float u[RS];
             load_row(slot, e, u);
-            float uy = 0.f;
-#pragma unroll
-            for (int j = 0; j < K; ++j) uy += u[j] * sfv[0][j];
+            const float uy = dotk<K>(u, sfv[0]);
             r[e] = __fsub_rn(xh[e], uy);
             float tw, g;
             penalty_t<PM>(r[e], w[e], a, tw, g);
@@ -433,9 +453,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
             for (int e = 0; e < 4; ++e) {
               float u[RS];
               load_row(slot, e, u);
-              float d = 0.f;
-#pragma unroll
-              for (int j = 0; j < K; ++j) d += u[j] * sfv[1][j];
+              const float d = dotk<K>(u, sfv[1]);
               ud[e] = d;
               // trial costs for every window step; the gradient only for the
               // speculative pair (same arithmetic as penalty_t, split)
@@ -533,12 +551,8 @@ __global__ void __launch_bounds__(TM_NT, 1)
             float tw, g;
             penalty_t<PM>(r[e], w[e], a, tw, g);
             const float eta = -g;  // cost.py:103-112
-            float uv = 0.f, ug = 0.f;
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-              uv += u[j] * sfv[2][j];
-              ug += u[j] * sfv[3][j];
-            }
+            const float uv = dotk<K>(u, sfv[2]);
+            const float ug = dotk<K>(u, sfv[3]);
             coef = ga * uv - gsn * ((eta - ug) / ln);
           }
 #pragma unroll
@@ -559,9 +573,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         uint32_t nl = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          float acc = 0.f;
-#pragma unroll
-          for (int j = 0; j < K; ++j) acc += up[e][j] * sfv[0][j];
+          const float acc = dotk<K>(up[e], sfv[0]);
           bgn[e] = acc;
           rr[e] = __fsub_rn(xh[e], acc);
           if (pix + e < a.P && fabs((double)rr[e]) >= a.delta) nl |= 1u << (8 * e);
