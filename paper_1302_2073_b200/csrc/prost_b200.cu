@@ -577,7 +577,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
         h->resident_ops_K = K;
         ALLOC(rbar, (size_t)sms * sizeof(unsigned));
         ALLOC(rpart, (size_t)2 * sms * RES_RNV_MAX * sizeof(double));
-        ALLOC(rprof, (size_t)sms * 8 * sizeof(unsigned long long));
+        ALLOC(rprof, (size_t)sms * PROF_N * sizeof(unsigned long long));
       }
       cudaGetLastError();
       break;
@@ -613,7 +613,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
         h->resident_ops_K = K;
         ALLOC(rbar, (size_t)sms * sizeof(unsigned));
         ALLOC(rpart, (size_t)2 * sms * RES_RNV_MAX * sizeof(double));
-        ALLOC(rprof, (size_t)sms * 8 * sizeof(unsigned long long));
+        ALLOC(rprof, (size_t)sms * PROF_N * sizeof(unsigned long long));
       }
       cudaGetLastError();
     }
@@ -985,16 +985,16 @@ int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n) {
   CK(cudaSetDevice(h->device));
   CK(cudaDeviceSynchronize());
   const int ctas = h->rT * h->rG;
-  std::vector<unsigned long long> v((size_t)ctas * 8);
+  std::vector<unsigned long long> v((size_t)ctas * PROF_N);
   CK(cudaMemcpy(v.data(), h->rprof, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   // per-CTA means of the counters of the last profiled launch, then the max total
   for (int c = 0; c < ctas; ++c)
-    for (int i = 0; i < 8 && i < n; ++i) out[i] += (int64_t)v[(size_t)c * 8 + i];
-  for (int i = 0; i < 8 && i < n; ++i) out[i] /= ctas;
-  if (n > 8) {
+    for (int i = 0; i < PROF_N && i < n; ++i) out[i] += (int64_t)v[(size_t)c * PROF_N + i];
+  for (int i = 0; i < PROF_N && i < n; ++i) out[i] /= ctas;
+  if (n >= PROF_N) {
     unsigned long long mx = 0;
-    for (int c = 0; c < ctas; ++c) mx = std::max(mx, v[(size_t)c * 8]);
-    out[8] = (int64_t)mx;
+    for (int c = 0; c < ctas; ++c) mx = std::max(mx, v[(size_t)c * PROF_N]);
+    out[PROF_N - 1] = (int64_t)mx;
   }
   return PROST_OK;
 }

@@ -35,7 +35,11 @@ struct RArgs {
 };
 
 // Timing counters of one CTA (thread 0, %globaltimer ns): see PROF_* below.
-enum { PROF_TOTAL = 0, PROF_BARRIER, PROF_SLOTS, PROF_LOGIC, PROF_PREFETCH, PROF_NSUMS, PROF_ROUNDS };
+enum {
+  PROF_TOTAL = 0, PROF_BARRIER, PROF_SLOTS, PROF_LOGIC, PROF_PREFETCH, PROF_NSUMS, PROF_ROUNDS,
+  PROF_T_STATS, PROF_T_PASS0, PROF_T_ITER, PROF_T_GEO,  // phase wall times (k_tmem)
+  PROF_N = 16
+};
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -241,8 +245,8 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ A
   uint64_t* mbar = reinterpret_cast<uint64_t*>(Rm + K * K);
 
   unsigned epoch = 0;
-  __shared__ unsigned long long sprof[8];
-  if (tid < 8) sprof[tid] = 0;
+  __shared__ unsigned long long sprof[PROF_N];
+  if (tid < PROF_N) sprof[tid] = 0;
   const unsigned long long t_start = gtimer();
 #define LOGIC(call)                                                    \
   do {                                                                 \
@@ -669,7 +673,7 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ A
   }
   if (ra.prof && tid == 0) {
     sprof[PROF_TOTAL] = gtimer() - t_start;
-    for (int i = 0; i < 8; ++i) ra.prof[(size_t)blockIdx.x * 8 + i] = sprof[i];
+    for (int i = 0; i < PROF_N; ++i) ra.prof[(size_t)blockIdx.x * PROF_N + i] = sprof[i];
   }
 #undef LOGIC
 }

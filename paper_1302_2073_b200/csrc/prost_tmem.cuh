@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
   constexpr int RS = Geo::RS, QW = Geo::QW, QT = Geo::QT;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ unsigned s_tbase;
-  __shared__ unsigned long long sprof[8];
+  __shared__ unsigned long long sprof[PROF_N];
   __shared__ float sfv[4][K];  // fp32 copies of y, d, v, grad for the per-element math
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
   double* red = wred + (size_t)(TM_NT / 32) * RES_RNV_MAX;
   Ctl* cs = reinterpret_cast<Ctl*>(red + RES_RNV_MAX);
 
-  if (tid < 8) sprof[tid] = 0;
+  if (tid < PROF_N) sprof[tid] = 0;
   const unsigned long long t_start = gtimer();
   // TMEM: 512 columns, allocated by warp 0
   if (warp == 0) {
@@ -217,6 +217,15 @@ __global__ void __launch_bounds__(TM_NT, 1)
       if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += gtimer() - tw0;
     }
 
+    unsigned long long tph = (ra.prof && tid == 0) ? gtimer() : 0;
+#define PHASE_MARK(idx)                              \
+  do {                                               \
+    if (ra.prof && tid == 0) {                       \
+      const unsigned long long tn = gtimer();        \
+      sprof[idx] += tn - tph;                        \
+      tph = tn;                                      \
+    }                                                \
+  } while (0)
     // ---- frame start: running statistics (pipeline.py:120-140) -------------
     const bool upd = a.pipeline && !cs->frozen && cs->frame_index < a.i_init;
     if (upd) {
@@ -330,6 +339,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
       }
     }
 
+    PHASE_MARK(PROF_T_STATS);
     if (cs->status == ST_OK) {
       // ---- pass 0: r = x - U y, cost, coordinate gradient (fit.py:96-104) ---
       {
@@ -366,6 +376,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         LOGIC(after_pass0<K>(cs, a, s, tid, red));
         __syncthreads();
       }
+      PHASE_MARK(PROF_T_PASS0);
 
       // ---- CG iterations (fit.py:108-144) -----------------------------------
       while (cs->status == ST_OK && cs->active) {
@@ -525,6 +536,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
         __syncthreads();
       }
     }
+    PHASE_MARK(PROF_T_ITER);
 
     if (cs->status == ST_OK) {
       // ---- geodesic step + relabel (manifold.py:116-197, tracker.py:146-147) ---
@@ -596,6 +608,8 @@ __global__ void __launch_bounds__(TM_NT, 1)
 
     // ---- commit the control block (one writer per stream) ------------------
     __syncthreads();
+    PHASE_MARK(PROF_T_GEO);
+#undef PHASE_MARK
     if (rank == 0 && tid < (int)(sizeof(Ctl) / 8))
       reinterpret_cast<double*>(a.ctl + s)[tid] = reinterpret_cast<const double*>(cs)[tid];
     __syncthreads();
@@ -604,7 +618,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
 #undef SYNC_FLOATS
   if (ra.prof && tid == 0) {
     sprof[PROF_TOTAL] = gtimer() - t_start;
-    for (int i = 0; i < 8; ++i) ra.prof[(size_t)blockIdx.x * 8 + i] = sprof[i];
+    for (int i = 0; i < PROF_N; ++i) ra.prof[(size_t)blockIdx.x * PROF_N + i] = sprof[i];
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

@@ -323,11 +323,15 @@ class NativeTracker:
 
     def resident_counters(self) -> dict:
         """Per-CTA mean timings (us) of the last profiled resident launch."""
-        out = (ctypes.c_int64 * 9)()
-        self._check(self._lib.prost_resident_counters(self._h, out, 9), "resident_counters")
-        names = ("kernel_us", "barrier_us", "slots_us", "logic_us", "prefetch_us")
+        n = 16
+        out = (ctypes.c_int64 * n)()
+        self._check(self._lib.prost_resident_counters(self._h, out, n), "resident_counters")
+        names = ("kernel_us", "barrier_us", "slots_us", "logic_us", "load_us")
         d = {nm: out[i] / 1e3 for i, nm in enumerate(names)}
-        d.update(team_sums=int(out[5]), rounds=int(out[6]), slowest_kernel_us=out[8] / 1e3)
+        d.update(team_sums=int(out[5]), rounds=int(out[6]), slowest_kernel_us=out[n - 1] / 1e3)
+        for i, nm in ((7, "phase_stats_us"), (8, "phase_pass0_us"), (9, "phase_iter_us"),
+                      (10, "phase_geo_us")):
+            d[nm] = out[i] / 1e3
         return d
 
     def set_wave(self, streams: int) -> None:
