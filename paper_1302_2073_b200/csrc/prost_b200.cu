@@ -78,6 +78,10 @@ struct prost_handle {
   size_t stage_bytes = 0;
   long long launches = 0;
   bool maybe_cold = true;
+  // upper bound on every stream's steps-since-QR before the next push: the
+  // periodic re-orthonormalization kernels are launched only when it can be due
+  long long qr_bound = 0;
+  bool qr_due = true;
   // optional per-phase timing (prost_profile)
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -194,6 +198,18 @@ struct PhaseTimer {
   }
 };
 
+// 3x3 majority filter of the raw labels into a.mask_out (pipeline.py:215-228)
+void launch_median(prost_handle* h, const Args& a, cudaStream_t st, int sw) {
+  if (h->prm.width % 4 == 0 && ((uintptr_t)a.mask_out & 3) == 0) {
+    const int nw = h->P / 4;
+    const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
+    k_median4<<<mg, NT, 0, st>>>(a);
+  } else {
+    const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), sw);
+    k_median<<<mg, NT, 0, st>>>(a);
+  }
+}
+
 #define LAUNCH(phase, ...)                  \
   do {                                      \
     PhaseTimer pt_(h, st, phase);           \
@@ -217,12 +233,11 @@ struct Impl {
       LAUNCH(PROST_PH_GRADFB, (k_gradfb<T, K, VEC><<<grid, NT, 0, st>>>(a)));
     }
     LAUNCH(PROST_PH_GEO, (k_geo<T, K, VEC, false><<<grid, NT, 0, st>>>(a)));
-    LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
-    LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
-    if (a.mask_out) {
-      const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), sw);
-      LAUNCH(PROST_PH_MEDIAN, (k_median<<<mg, NT, 0, st>>>(a)));
+    if (h->qr_due) {
+      LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+      LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
     }
+    if (a.mask_out) LAUNCH(PROST_PH_MEDIAN, launch_median(h, a, st, sw));
     h->launches += n;
   }
 
@@ -566,18 +581,25 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
       const int qpc = ((nq + G - 1) / G + 3) / 4 * 4;
       if ((nq + qpc - 1) / qpc != G) continue;
       const size_t sm = to.smem(qpc);
-      if (sm > 227 * 1024) continue;
-      if (to.prepare(sm) == cudaSuccess && to.occupancy(sm) >= 1) {
+      if (sm > (size_t)227 * 1024) continue;
+      if (to.prepare(sm) != cudaSuccess || to.occupancy(sm) < TM_CPS) {
+        if (getenv("PROST_DEBUG"))
+          fprintf(stderr, "prost: tmem G=%d qpc=%d smem=%zu rejected (%s, occupancy %d)\n", G, qpc, sm,
+                  cudaGetErrorString(cudaGetLastError()), to.occupancy(sm));
+        cudaGetLastError();
+        continue;  // TM_CPS CTAs of this size do not fit an SM: larger team
+      }
+      {
         h->tmem = true;
         h->rqpc = qpc;
         h->rnt = TM_NT;
         h->rsmem = sm;
         h->rG = G;
-        h->rT = std::min(h->S, sms / G);
+        h->rT = std::min(h->S, sms * TM_CPS / G);
         h->resident_ops_K = K;
-        ALLOC(rbar, (size_t)sms * sizeof(unsigned));
-        ALLOC(rpart, (size_t)2 * sms * RES_RNV_MAX * sizeof(double));
-        ALLOC(rprof, (size_t)sms * PROF_N * sizeof(unsigned long long));
+        ALLOC(rbar, (size_t)sms * TM_CPS * sizeof(unsigned));
+        ALLOC(rpart, (size_t)2 * sms * TM_CPS * RES_RNV_MAX * sizeof(double));
+        ALLOC(rprof, (size_t)sms * TM_CPS * PROF_N * sizeof(unsigned long long));
       }
       cudaGetLastError();
       break;
@@ -694,6 +716,7 @@ int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const
     for (int j = 0; j < k; ++j) c.y[j] = y[j];
   c.frame_index = frame_index;
   c.since_qr = steps_since_qr;
+  h->qr_bound = std::max<long long>(h->qr_bound, steps_since_qr);
   c.status = ST_OK;
   c.active = 0;
   CK(cudaMemcpy(h->ctl + stream, &c, sizeof c, cudaMemcpyHostToDevice));
@@ -789,6 +812,19 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
     return fail(h, PROST_ERR_CONFIG, "unknown frame dtype %d", dtype);
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  // A QR is due in this push only for a stream whose steps-since-QR is already
+  // QR_EVERY - 1 (manifold.py:192).  Near that bound, refresh it from the
+  // device (one small synchronous read every ~QR_EVERY frames).
+  if (h->qr_bound >= QR_EVERY - 1) {
+    std::vector<Ctl> cs(h->S);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(cs.data(), h->ctl, (size_t)h->S * sizeof(Ctl), cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (const Ctl& c : cs) mx = std::max(mx, c.since_qr);
+    h->qr_bound = mx;
+  }
+  h->qr_due = h->qr_bound >= QR_EVERY - 1;
+  h->qr_bound += 1;
   const bool same = (dtype == PROST_F64) == h->fp64 && dtype != PROST_U8;
   const bool dense = h->P == h->Pp;
   const void* xdev = h->x;
@@ -846,11 +882,10 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
         CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
       ++n;
     }
-    if (h->tmem) h->ops.qr(h, a, st, h->S);  // exits at once unless a QR is due
+    if (h->tmem && h->qr_due) h->ops.qr(h, a, st, h->S);  // per stream: exits unless due
     if (a.mask_out) {
-      const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), h->S);
       PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
-      k_median<<<mg, NT, 0, st>>>(a);
+      launch_median(h, a, st, h->S);
       ++n;
     }
     h->launches += n;

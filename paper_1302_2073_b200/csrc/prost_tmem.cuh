@@ -19,7 +19,18 @@
 
 namespace prost {
 
-constexpr int TM_NT = 512;  // threads per CTA: 16 warps = 4 per TMEM lane quarter
+#ifndef PROST_TM_NT
+#define PROST_TM_NT 512
+#endif
+#ifndef PROST_TM_CPS
+#define PROST_TM_CPS 1
+#endif
+// threads per CTA: 4 warps per 128-column TMEM block (one per lane quarter);
+// the CTA allocates TM_NT columns.  TM_CPS CTAs share an SM (their teams
+// interleave: one computes while the other waits on a team barrier).
+constexpr int TM_NT = PROST_TM_NT;
+constexpr int TM_CPS = PROST_TM_CPS;
+static_assert(TM_NT == 128 || TM_NT == 256 || TM_NT == 512, "TMEM allocation is TM_NT columns");
 
 template <int K>
 struct TmemGeom {
@@ -70,7 +81,7 @@ __device__ __forceinline__ float dotk(const float* u, const float* v) {
 }
 
 template <int K, int PM>
-__global__ void __launch_bounds__(TM_NT, 1)
+__global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
   constexpr int RS = Geo::RS, QW = Geo::QW, QT = Geo::QT;
@@ -102,10 +113,10 @@ __global__ void __launch_bounds__(TM_NT, 1)
 
   if (tid < PROF_N) sprof[tid] = 0;
   const unsigned long long t_start = gtimer();
-  // TMEM: 512 columns, allocated by warp 0
+  // TMEM: TM_NT columns, allocated by warp 0
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-        smem_addr(&s_tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_addr(&s_tbase)), "n"(TM_NT));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -622,7 +633,7 @@ __global__ void __launch_bounds__(TM_NT, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tbase));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tbase), "n"(TM_NT));
 }
 
 }  // namespace prost
