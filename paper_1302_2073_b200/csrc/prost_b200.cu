@@ -309,6 +309,7 @@ struct TmOps {
   int (*occupancy)(size_t smem);
   size_t (*smem)(int qpc);
   int qt;  // row groups per thread held in TMEM
+  void (*describe)();
 };
 
 template <int K, int PM>
@@ -317,8 +318,14 @@ struct Tm {
     Args aa = a;
     RArgs rr = ra;
     void* args[] = {&aa, &rr};
-    return cudaLaunchCooperativeKernel((const void*)k_tmem<K, PM>, dim3(ra.T * ra.G), dim3(TM_NT),
-                                       args, smem, st);
+    if (TM_CPS == 1)
+      return cudaLaunchCooperativeKernel((const void*)k_tmem<K, PM>, dim3(ra.T * ra.G), dim3(TM_NT),
+                                         args, smem, st);
+    // The occupancy calculator reports one CTA per SM for any kernel that
+    // allocates tensor memory, so a cooperative launch of TM_CPS CTAs per SM is
+    // refused; the hardware co-schedules them (tools/probe/coresid_probe.cu),
+    // and the grid is sized to the chip, so every CTA is resident at once.
+    return cudaLaunchKernel((const void*)k_tmem<K, PM>, dim3(ra.T * ra.G), dim3(TM_NT), args, smem, st);
   }
   static cudaError_t prepare(size_t smem) {
     return cudaFuncSetAttribute(k_tmem<K, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -330,7 +337,15 @@ struct Tm {
     return nb;
   }
   static size_t smem(int qpc) { return tmem_smem<K>(qpc); }
-  static TmOps ops() { return TmOps{&launch, &prepare, &occupancy, &smem, TmemGeom<K>::QT}; }
+  static void describe() {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_tmem<K, PM>);
+    int nb0 = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, k_tmem<K, PM>, TM_NT, 0);
+    fprintf(stderr, "prost: k_tmem<%d> regs %d local %zu static smem %zu max threads %d; occupancy(smem 0) %d\n",
+            K, fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes, fa.maxThreadsPerBlock, nb0);
+  }
+  static TmOps ops() { return TmOps{&launch, &prepare, &occupancy, &smem, TmemGeom<K>::QT, &describe}; }
 };
 
 TmOps pick_tmem(int K, bool half) {
@@ -339,7 +354,7 @@ TmOps pick_tmem(int K, bool half) {
     case 8: return half ? Tm<8, PM_HALF>::ops() : Tm<8, PM_ANY>::ops();
     case 15: return half ? Tm<15, PM_HALF>::ops() : Tm<15, PM_ANY>::ops();
     case 16: return half ? Tm<16, PM_HALF>::ops() : Tm<16, PM_ANY>::ops();
-    default: return TmOps{nullptr, nullptr, nullptr, nullptr, 0};
+    default: return TmOps{nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   }
 }
 
@@ -575,14 +590,38 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   const bool eligible = !h->fp64 && h->C == 1 && K <= 16;
   const TmOps to = pick_tmem(K, params->p == 0.5);
   if (eligible && kpath == "tmem" && to.launch) {
-    // smallest team whose slice fits TMEM + shared memory: the most streams in flight
+    if (getenv("PROST_DEBUG")) to.describe();
+    // Team size: among the slices that fit TMEM + shared memory, the one with
+    // the most stream frames per unit time, teams / round time, with the round
+    // time modelled as a fixed part (reduction latency, ~1.5 slot sweeps as
+    // measured on C3) plus one part per row-group slot a thread walks (every
+    // thread of a CTA walks the same number of slots, so a slice just over a
+    // slot boundary costs a whole extra slot).  Depends on the stream shape
+    // and the chip only (not on n_streams): per-stream results do not depend
+    // on the batch.
     const int nq = h->Pp / 4;
+    int bestG = 0;
+    double best_cost = 0;
     for (int G = 1; G <= sms; ++G) {
       const int qpc = ((nq + G - 1) / G + 3) / 4 * 4;
       if ((nq + qpc - 1) / qpc != G) continue;
       const size_t sm = to.smem(qpc);
       if (sm > (size_t)227 * 1024) continue;
-      if (to.prepare(sm) != cudaSuccess || to.occupancy(sm) < TM_CPS) {
+      const double cost = (1.5 + (qpc + TM_NT - 1) / TM_NT) / (double)(sms * TM_CPS / G);
+      if (bestG == 0 || cost < best_cost) {
+        bestG = G;
+        best_cost = cost;
+      }
+    }
+    for (int G = bestG > 0 ? bestG : sms + 1; G <= sms; ++G) {
+      const int qpc = ((nq + G - 1) / G + 3) / 4 * 4;
+      if ((nq + qpc - 1) / qpc != G) continue;
+      const size_t sm = to.smem(qpc);
+      if (sm > (size_t)227 * 1024) continue;
+      const bool set = to.prepare(sm) == cudaSuccess;  // before the occupancy query
+      const bool fits = set && (TM_CPS == 1 ? to.occupancy(sm) >= 1
+                                            : (size_t)TM_CPS * (sm + 2048) <= (size_t)228 * 1024);
+      if (!fits) {
         if (getenv("PROST_DEBUG"))
           fprintf(stderr, "prost: tmem G=%d qpc=%d smem=%zu rejected (%s, occupancy %d)\n", G, qpc, sm,
                   cudaGetErrorString(cudaGetLastError()), to.occupancy(sm));

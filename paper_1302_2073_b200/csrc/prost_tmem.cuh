@@ -1,23 +1,34 @@
 // prost_tmem.cuh — the TMEM-resident frame kernel (k_tmem).
 //
-// Same team structure as k_resident (a persistent cooperative grid split into
-// T teams of G CTAs; a team owns one stream per round; the frame's dependent
-// reductions are team-wide sums through double-buffered global slots and a
-// release/acquire counter barrier, after which every CTA runs the scalar
-// logic itself).  The difference is where a CTA keeps its slice of U: each
-// thread owns QT row groups (4 rows x k values) in its lane of tensor memory
-// (written once per frame with tcgen05.st, read row by row with tcgen05.ld in
-// every phase), plus, when the slice is larger, row groups in shared memory.
-// With 256 KB of TMEM + shared memory per SM a C3 stream (76,800 x 15 fp32 =
-// 4.6 MB) fits on 13 SMs, so 11 streams are in flight at once, and U crosses
-// HBM exactly once each way per frame.  Working one row (k values) at a time
-// keeps the live basis registers at 16 instead of 4k.
+// A persistent grid split into T teams of G CTAs (one CTA per SM); a team owns
+// one stream per round.  The frame's dependent reductions are team-wide sums
+// through double-buffered global slots and a release/acquire counter barrier,
+// after which every CTA runs the scalar logic itself (prost_resident.cuh).
+//
+// Where the basis lives: each thread owns row groups (4 rows x k values) in
+// its lane of tensor memory (written once per frame with tcgen05.st, read one
+// row at a time with tcgen05.ld in every phase) and, when the slice is larger,
+// row groups in shared memory.  Per CTA that is 256 KB of TMEM + ~200 KB of
+// shared memory, so a C3 stream (76,800 x 15 fp32 = 4.6 MB) fits on 12 SMs and
+// 12 streams are in flight; U crosses HBM exactly once each way per frame.
+//
+// What is kept per row group besides U: the residual r and the last u_dir = U d
+// (shared memory).  The frame itself is re-read from global memory by the one
+// sweep that needs it (pass 0), and the relabel uses r' = r - coef (v . y)
+// (row i of U' is u_i + coef_i v^T), so no copy of the frame is kept on chip.
+// With k < 16 the per-coordinate weight w (1, omega, or 0 for padding) rides in
+// the unused 16th TMEM / shared-memory column of each row.
+//
+// Instruction economy: the sweeps are compile-time loops over the 4 rows of a
+// row group; TMEM and shared-memory row groups are separate loop instances; the
+// CG iteration sweep is instantiated per speculative-gradient window position;
+// an accepted step's residual update is applied by the next sweep that reads r.
 #pragma once
+
+#include <type_traits>
 
 #include "prost_resident.cuh"
 #include "tmem_io.cuh"
-
-namespace prost {
 
 #ifndef PROST_TM_NT
 #define PROST_TM_NT 512
@@ -25,9 +36,11 @@ namespace prost {
 #ifndef PROST_TM_CPS
 #define PROST_TM_CPS 1
 #endif
+
+namespace prost {
+
 // threads per CTA: 4 warps per 128-column TMEM block (one per lane quarter);
-// the CTA allocates TM_NT columns.  TM_CPS CTAs share an SM (their teams
-// interleave: one computes while the other waits on a team barrier).
+// the CTA allocates TM_NT columns.  TM_CPS CTAs may share an SM.
 constexpr int TM_NT = PROST_TM_NT;
 constexpr int TM_CPS = PROST_TM_CPS;
 static_assert(TM_NT == 128 || TM_NT == 256 || TM_NT == 512, "TMEM allocation is TM_NT columns");
@@ -36,17 +49,25 @@ template <int K>
 struct TmemGeom {
   // columns per row (power of two >= k: every tcgen05 access is width-aligned)
   static constexpr int RS = K <= 4 ? 4 : (K <= 8 ? 8 : 16);
-  static constexpr int QW = 4 * RS;        // columns per row group
-  static constexpr int QT = 128 / QW;      // row groups per thread in TMEM
+  static constexpr int QW = 4 * RS;     // columns per row group
+  static constexpr int QT = 128 / QW;   // row groups per thread in TMEM
+  static constexpr bool WCOL = K < RS;  // weight stored in column RS-1
+  // values reduced per team sum (largest: the CG iteration sweep)
+  static constexpr int NV0 = WC + WG * (K + 1);
+  static constexpr int NV1 = LSW > K + 3 ? LSW : K + 3;
+  static constexpr int NV = NV0 > NV1 ? NV0 : NV1;
 };
 
 // Dynamic shared memory of k_tmem<K> for qpc row groups per CTA.
 template <int K>
 __host__ __device__ constexpr size_t tmem_smem(int qpc) {
-  const int qs = qpc > TmemGeom<K>::QT * TM_NT ? qpc - TmemGeom<K>::QT * TM_NT : 0;
-  return (size_t)16 * TmemGeom<K>::RS * qs     // basis row groups kept in shared memory
-         + (size_t)qpc * (3 * 16 + 4)           // r, u_dir, normalized frame, labels
-         + (size_t)(TM_NT / 32 + 1) * RES_RNV_MAX * 8 + sizeof(Ctl) + 64;
+  using Geo = TmemGeom<K>;
+  const int qs = qpc > Geo::QT * TM_NT ? qpc - Geo::QT * TM_NT : 0;
+  const int qa = (qpc + TM_NT - 1) / TM_NT * TM_NT;  // r / u_dir arrays cover whole slots
+  return (size_t)16 * Geo::RS * qs                     // basis row groups kept in shared memory
+         + (size_t)qa * 32                             // r, u_dir
+         + (Geo::WCOL ? 0 : (size_t)qa * 4)            // label words
+         + (size_t)(TM_NT / 32 + 1) * Geo::NV * 8 + sizeof(Ctl) + 64;
 }
 
 template <int RS>
@@ -80,15 +101,43 @@ __device__ __forceinline__ float dotk(const float* u, const float* v) {
   return (p0 + p1) + (p2 + p3);
 }
 
+// Row access of one row group: TMEM (warp-collective tcgen05.ld) or shared memory.
+template <int RS>
+struct TmemRows {
+  unsigned taddr;
+  __device__ __forceinline__ void operator()(int e, float (&u)[RS]) const {
+    tmem_ld_row<RS>(taddr + e * RS, u);
+    tmem_wait_ld();
+  }
+};
+template <int RS>
+struct SmemRows {
+  const float4* base;  // row e, column group g at base[(e * RS/4 + g) * qs]
+  int qs;
+  bool ok;
+  __device__ __forceinline__ void operator()(int e, float (&u)[RS]) const {
+#pragma unroll
+    for (int g4 = 0; g4 < RS / 4; ++g4) {
+      const float4 t = ok ? base[(size_t)(e * (RS / 4) + g4) * qs] : make_float4(0.f, 0.f, 0.f, 0.f);
+      u[4 * g4] = t.x; u[4 * g4 + 1] = t.y; u[4 * g4 + 2] = t.z; u[4 * g4 + 3] = t.w;
+    }
+  }
+};
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
 template <int K, int PM>
 __global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
-  constexpr int RS = Geo::RS, QW = Geo::QW, QT = Geo::QT;
+  constexpr int RS = Geo::RS, QW = Geo::QW, QT = Geo::QT, NVM = Geo::NV;
+  constexpr bool WCOL = Geo::WCOL;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ unsigned s_tbase;
   __shared__ unsigned long long sprof[PROF_N];
   __shared__ float sfv[4][K];  // fp32 copies of y, d, v, grad for the per-element math
+  __shared__ float s_vy;       // v . y of the geodesic step (relabel without the frame)
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -97,26 +146,29 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   const int q0 = rank * qpc;
   const int qcount = max(0, min(qpc, nq - q0));
   const int nslots = (qcount + TM_NT - 1) / TM_NT;  // uniform across the CTA
+  const int nst = nslots < QT ? nslots : QT;        // TMEM slots in use
   const int qs = qpc > QT * TM_NT ? qpc - QT * TM_NT : 0;
+  const int qa = (qpc + TM_NT - 1) / TM_NT * TM_NT;
 
   // basis rows kept in shared memory: [row e][4-column group][row group] float4,
   // so a thread reads one row with RS/4 conflict-free 16-byte loads
-  float4* sU = reinterpret_cast<float4*>(smem_raw);         // [4][RS/4][qs]
-  float4* sR = sU + (size_t)RS * qs;                        // [qpc] residual
-  float4* sD = sR + qpc;                                    // [qpc] u_dir
-  float4* sX = sD + qpc;                                    // [qpc] normalized frame
-  uint32_t* sL = reinterpret_cast<uint32_t*>(sX + qpc);     // [qpc] label bytes
-  const float* Mg = static_cast<const float*>(a.mean);      // running mean stays in global/L2
-  double* wred = reinterpret_cast<double*>(sL + ((qpc + 1) / 2) * 2);
-  double* red = wred + (size_t)(TM_NT / 32) * RES_RNV_MAX;
-  Ctl* cs = reinterpret_cast<Ctl*>(red + RES_RNV_MAX);
+  float4* sU = reinterpret_cast<float4*>(smem_raw);     // [4][RS/4][qs]
+  float4* sR = sU + (size_t)RS * qs;                    // [qa] residual
+  float4* sD = sR + qa;                                 // [qa] u_dir
+  uint32_t* sL = reinterpret_cast<uint32_t*>(sD + qa);  // [qa] label bytes (!WCOL)
+  double* wred = reinterpret_cast<double*>(sL + (WCOL ? 0 : qa));
+  double* red = wred + (size_t)(TM_NT / 32) * NVM;
+  Ctl* cs = reinterpret_cast<Ctl*>(red + NVM);
+  const float* Mg = static_cast<const float*>(a.mean);
+  const float* Xg = static_cast<const float*>(a.x);
 
   if (tid < PROF_N) sprof[tid] = 0;
   const unsigned long long t_start = gtimer();
   // TMEM: TM_NT columns, allocated by warp 0
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-        smem_addr(&s_tbase)), "n"(TM_NT));
+                     smem_addr(&s_tbase)),
+                 "n"(TM_NT));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -147,25 +199,19 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     if (ra.prof && tid == 0) sprof[PROF_LOGIC] += gtimer() - tl0;          \
   } while (0)
 
-  // One row (e) of row group `slot`: the k basis values of that coordinate.
-  // TMEM rows are read by the whole warp (tcgen05 is warp-collective).
-  auto load_row = [&](int slot, int e, float (&u)[RS]) {
-    if (slot < QT) {
-      tmem_ld_row<RS>(tbase + slot * QW + e * RS, u);
-      tmem_wait_ld();
-    } else {
-      const int i = slot * TM_NT + tid - QT * TM_NT;
-      const bool ok = slot * TM_NT + tid < qcount;
-      const float4* rp = sU + (size_t)(e * (RS / 4)) * qs + i;
-#pragma unroll
-      for (int g4 = 0; g4 < RS / 4; ++g4) {
-        const float4 t = ok ? rp[(size_t)g4 * qs] : make_float4(0.f, 0.f, 0.f, 0.f);
-        u[4 * g4] = t.x; u[4 * g4 + 1] = t.y; u[4 * g4 + 2] = t.z; u[4 * g4 + 3] = t.w;
-      }
+  // Visit every row group of this thread: body(qi, rows).  TMEM row groups
+  // first, then shared-memory ones (separate instances of the body).
+  auto sweep = [&](auto&& body) {
+    for (int slot = 0; slot < nst; ++slot)
+      body(slot * TM_NT + tid, TmemRows<RS>{tbase + (unsigned)(slot * QW)});
+    for (int slot = QT; slot < nslots; ++slot) {
+      const int i = (slot - QT) * TM_NT + tid;
+      body(slot * TM_NT + tid, SmemRows<RS>{sU + i, qs, i < qs});
     }
   };
   const float omega = a.omegaf;
-  auto weights = [&](int qi, float (&w)[4]) {
+  // weights of a row group from the label words (layout without a weight column)
+  auto lab_weights = [&](int qi, float (&w)[4]) {
     const uint32_t lb = qi < qcount ? sL[qi] : 0u;
     const int pix = (q0 + qi) * 4;
 #pragma unroll
@@ -174,9 +220,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   };
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
 
-  // Stagger the teams: rounds are near-identical in length, so without an
-  // offset all teams load (and store) their slices at the same moment and the
-  // HBM traffic comes in bursts.  Odd teams start half a round late (ra.stagger_ns).
+  // Stagger the teams (optional): odd teams start ra.stagger_ns late.
   if ((team & 1) && ra.stagger_ns > 0) {
     const unsigned long long t0 = gtimer();
     while (gtimer() - t0 < (unsigned long long)ra.stagger_ns) __nanosleep(1000);
@@ -184,22 +228,21 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 
   for (int s = team; s < ra.S; s += T) {
     if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
-    // ---- load this stream's slice: U -> TMEM / shared, frame, mean, labels ---
+    const size_t so = (size_t)s * a.np;  // this stream's plane offset
+    // ---- load this stream's slice: U (+ weights) -> TMEM / shared memory ----
     {
       const unsigned long long tw0 = (ra.prof && tid == 0) ? gtimer() : 0;
       const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
       for (int slot = 0; slot < nslots; ++slot) {
         const int qi = slot * TM_NT + tid;  // row group within the slice
         const bool ok = qi < qcount;
-        const size_t off = (size_t)(q0 + qi) * 4;
+        const int pix = (q0 + qi) * 4;
         float4 p[K];
 #pragma unroll
         for (int j = 0; j < K; ++j)
-          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + off)) : z4;
-        if (ok) {
-          sX[qi] = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + (size_t)s * a.np + off));
-          sL[qi] = *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + (q0 + qi) * 4);
-        }
+          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + pix)) : z4;
+        const uint32_t lb = ok ? *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + pix) : 0u;
+        if (!WCOL) sL[qi] = lb;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float row[RS];
@@ -208,6 +251,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             const float4 t = j < K ? p[j] : z4;
             row[j] = e == 0 ? t.x : (e == 1 ? t.y : (e == 2 ? t.z : t.w));
           }
+          if (WCOL)
+            row[RS - 1] = (ok && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
           if (slot < QT) {
             tmem_st_row<RS>(tbase + slot * QW + e * RS, row);
           } else if (ok) {
@@ -244,9 +289,9 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       for (int slot = 0; slot < nslots; ++slot) {
         const int qi = slot * TM_NT + tid;
         if (qi >= qcount) continue;
-        float xv[4];
-        f4(sX[qi], xv);
         const int pix = (q0 + qi) * 4;
+        float xv[4];
+        f4(*reinterpret_cast<const float4*>(Xg + so + pix), xv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (pix + e < a.P) {
@@ -291,52 +336,56 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     }
     __syncthreads();
 
-    // normalize the frame in place; fold the running mean (pipeline.py:148-156)
-    bool bad = false;
-    if (cs->status == ST_OK) {
-      const float stdv = (float)cs->std_cur, seen = (float)cs->pseen;
-      for (int slot = 0; slot < nslots; ++slot) {
-        const int qi = slot * TM_NT + tid;
-        if (qi >= qcount) continue;
-        const int pix = (q0 + qi) * 4;
-        float xv[4], mv[4], xh[4];
-        f4(sX[qi], xv);
-        f4(a.pipeline ? *reinterpret_cast<const float4*>(Mg + (size_t)s * a.np + pix) : z4, mv);
+    // normalized frame of a row group (pipeline.py:148-156); the sweep that
+    // owns this frame's running-mean update writes the mean back
+    const float stdv = (float)cs->std_cur, seen = (float)cs->pseen;
+    auto xhat = [&](int qi, bool wr, float (&xh)[4], bool& bad) {
+      const bool ok = qi < qcount;
+      const int pix = (q0 + qi) * 4;
+      float xv[4];
+      f4(ok ? *reinterpret_cast<const float4*>(Xg + so + pix) : z4, xv);
+      if (a.pipeline) {
+        float mv[4];
+        f4(ok ? *reinterpret_cast<const float4*>(Mg + so + pix) : z4, mv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           bad |= !isfinite(xv[e]);
-          if (a.pipeline) {
-            if (upd) mv[e] = __fadd_rn(mv[e], __fdiv_rn(__fsub_rn(xv[e], mv[e]), seen));
-            xh[e] = __fdiv_rn(__fsub_rn(xv[e], mv[e]), stdv);
-          } else {
-            xh[e] = xv[e];
-          }
+          if (wr) mv[e] = __fadd_rn(mv[e], __fdiv_rn(__fsub_rn(xv[e], mv[e]), seen));
+          xh[e] = __fdiv_rn(__fsub_rn(xv[e], mv[e]), stdv);
           if (pix + e >= a.P) xh[e] = 0.f;
         }
-        sX[qi] = make_float4(xh[0], xh[1], xh[2], xh[3]);
-        if (upd) {
-          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + (size_t)s * a.np + pix) =
+        if (wr && ok)
+          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + so + pix) =
               make_float4(mv[0], mv[1], mv[2], mv[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bad |= !isfinite(xv[e]);
+          xh[e] = pix + e < a.P ? xv[e] : 0.f;
         }
       }
+    };
 
+    if (cs->status == ST_OK) {
+      bool bad = false;
+      bool mean_pending = upd;  // running-mean update not yet written this frame
       // ---- cold start y = U^T x (fit.py:86-87) -------------------------------
       if (cs->frame_index == 0) {
         float pk[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) pk[j] = 0.f;
-        for (int slot = 0; slot < nslots; ++slot) {
-          const int qi = slot * TM_NT + tid;
+        sweep([&](int qi, const auto& rows) {
           float xh[4];
-          f4(qi < qcount ? sX[qi] : z4, xh);
+          xhat(qi, upd, xh, bad);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float u[RS];
-            load_row(slot, e, u);
+            rows(e, u);
 #pragma unroll
             for (int j = 0; j < K; ++j) pk[j] += u[j] * xh[e];
           }
-        }
+        });
+        mean_pending = false;
         stage_floats<K>(pk, wred, K + 1, 0);
         rstage(bad ? 1.0 : 0.0, wred, K, K + 1);
         team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
@@ -348,28 +397,25 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         }
         __syncthreads();
       }
-    }
+      PHASE_MARK(PROF_T_STATS);
 
-    PHASE_MARK(PROF_T_STATS);
-    if (cs->status == ST_OK) {
       // ---- pass 0: r = x - U y, cost, coordinate gradient (fit.py:96-104) ---
-      {
+      if (cs->status == ST_OK) {
         double cost = 0.0;
         float pk[K + 1];
 #pragma unroll
         for (int j = 0; j <= K; ++j) pk[j] = 0.f;
-        for (int slot = 0; slot < nslots; ++slot) {
-          const int qi = slot * TM_NT + tid;
+        sweep([&](int qi, const auto& rows) {
           float xh[4], w[4], r[4];
-          f4(qi < qcount ? sX[qi] : z4, xh);
-          weights(qi, w);
+          xhat(qi, mean_pending, xh, bad);
+          if (!WCOL) lab_weights(qi, w);
           float tc = 0.f;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float u[RS];
-            load_row(slot, e, u);
-            const float uy = dotk<K>(u, sfv[0]);
-            r[e] = __fsub_rn(xh[e], uy);
+            rows(e, u);
+            if (WCOL) w[e] = u[RS - 1];
+            r[e] = __fsub_rn(xh[e], dotk<K>(u, sfv[0]));
             float tw, g;
             penalty_t<PM>(r[e], w[e], a, tw, g);
             tc += tw;
@@ -378,8 +424,9 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
           }
           cost += (double)tc;
-          if (qi < qcount) sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
-        }
+          sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
+          sD[qi] = z4;
+        });
         rstage(cost, wred, 0, K + 3);
         stage_floats<K + 1>(pk, wred, K + 3, 1);
         rstage(bad ? 1.0 : 0.0, wred, K + 2, K + 3);
@@ -387,101 +434,116 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         LOGIC(after_pass0<K>(cs, a, s, tid, red));
         __syncthreads();
       }
-      PHASE_MARK(PROF_T_PASS0);
+    } else {
+      PHASE_MARK(PROF_T_STATS);
+    }
+    PHASE_MARK(PROF_T_PASS0);
 
-      // ---- CG iterations (fit.py:108-144) -----------------------------------
-      while (cs->status == ST_OK && cs->active) {
-        if (cs->need_lsfb) {
-          const int base = cs->ls_next;
-          const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
-          const double al0 = alpha_at(a, base);
-          float cst[LSW];
+    // ---- CG iterations (fit.py:108-144) -------------------------------------
+    // pend_alpha (an accepted step not yet applied to r) is applied by the
+    // next sweep that reads r: the iteration sweep or the geodesic sweep.
+    while (cs->status == ST_OK && cs->active) {
+      if (cs->need_lsfb) {
+        const int base = cs->ls_next;
+        const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
+        const double al0 = alpha_at(a, base);
+        float cst[LSW];
 #pragma unroll
-          for (int m = 0; m < LSW; ++m) cst[m] = 0.f;
-          for (int slot = 0; slot < nslots; ++slot) {
-            const int qi = slot * TM_NT + tid;
-            if (qi >= qcount) continue;
-            float r[4], ud[4], w[4];
-            f4(sR[qi], r);
-            f4(sD[qi], ud);
-            weights(qi, w);
-            double al = al0;
+        for (int m = 0; m < LSW; ++m) cst[m] = 0.f;
+        sweep([&](int qi, const auto& rows) {
+          float r[4], ud[4], w[4];
+          f4(sR[qi], r);
+          f4(sD[qi], ud);
+          if (WCOL) {
 #pragma unroll
-            for (int m = 0; m < LSW; ++m) {
-              if (m < cnt) {
+            for (int e = 0; e < 4; ++e) {
+              float u[RS];
+              rows(e, u);
+              w[e] = u[RS - 1];
+            }
+          } else {
+            lab_weights(qi, w);
+          }
+          double al = al0;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  float tw, g;
-                  penalty_t<PM>(trial(r[e], (float)al, ud[e]), w[e], a, tw, g);
-                  cst[m] += tw;
-                }
+          for (int m = 0; m < LSW; ++m) {
+            if (m < cnt) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float tw, g;
+                penalty_t<PM>(trial(r[e], (float)al, ud[e]), w[e], a, tw, g);
+                cst[m] += tw;
               }
-              al *= a.shrink;
             }
+            al *= a.shrink;
           }
+        });
 #pragma unroll
-          for (int m = 0; m < LSW; ++m) rstage((double)cst[m], wred, m, LSW);
-          team_sum(ra, team, rank, wred, LSW, red, epoch, sprof);
-          LOGIC(after_lsfb(cs, a, s, tid, red, base));
-        } else if (cs->need_gradfb) {
-          const float al = (float)cs->acc_alpha;
-          float pk[K + 1];
+        for (int m = 0; m < LSW; ++m) rstage((double)cst[m], wred, m, LSW);
+        team_sum(ra, team, rank, wred, LSW, red, epoch, sprof);
+        LOGIC(after_lsfb(cs, a, s, tid, red, base));
+      } else if (cs->need_gradfb) {
+        const float al = (float)cs->acc_alpha;
+        float pk[K + 1];
 #pragma unroll
-          for (int j = 0; j <= K; ++j) pk[j] = 0.f;
-          for (int slot = 0; slot < nslots; ++slot) {
-            const int qi = slot * TM_NT + tid;
-            float r[4], ud[4], w[4];
-            f4(qi < qcount ? sR[qi] : z4, r);
-            f4(qi < qcount ? sD[qi] : z4, ud);
-            weights(qi, w);
+        for (int j = 0; j <= K; ++j) pk[j] = 0.f;
+        sweep([&](int qi, const auto& rows) {
+          float r[4], ud[4], w[4];
+          f4(sR[qi], r);
+          f4(sD[qi], ud);
+          if (!WCOL) lab_weights(qi, w);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float u[RS];
+            rows(e, u);
+            if (WCOL) w[e] = u[RS - 1];
+            float tw, g;
+            penalty_t<PM>(trial(r[e], al, ud[e]), w[e], a, tw, g);
+            pk[K] += g * g;
+#pragma unroll
+            for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
+          }
+        });
+        stage_floats<K + 1>(pk, wred, K + 1, 0);
+        team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
+        LOGIC(after_gradfb<K>(cs, a, s, tid, red));
+      } else {
+        constexpr int NV = WC + WG * (K + 1);
+        const int wlo = cs->gwin_lo;
+        const float pa = (float)cs->pend_alpha;
+        float al[WC];
+        {
+          double v = a.step0;
+#pragma unroll
+          for (int m = 0; m < WC; ++m) {
+            al[m] = (float)v;
+            v *= a.shrink;
+          }
+        }
+        float cst[WC];
+        float pk[WG * (K + 1)];
+#pragma unroll
+        for (int m = 0; m < WC; ++m) cst[m] = 0.f;
+#pragma unroll
+        for (int i = 0; i < WG * (K + 1); ++i) pk[i] = 0.f;
+        // trial costs for every window step; the gradient only for the
+        // speculative pair [WLO, WLO + WG) (same arithmetic as penalty_t)
+        auto iter_sweep = [&](auto wlo_c) {
+          constexpr int WLO = decltype(wlo_c)::value;
+          sweep([&](int qi, const auto& rows) {
+            float r[4], w[4], udo[4], ud[4];
+            f4(sR[qi], r);
+            f4(sD[qi], udo);
+            if (!WCOL) lab_weights(qi, w);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               float u[RS];
-              load_row(slot, e, u);
-              float tw, g;
-              penalty_t<PM>(trial(r[e], al, ud[e]), w[e], a, tw, g);
-              pk[K] += g * g;
-#pragma unroll
-              for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
-            }
-          }
-          stage_floats<K + 1>(pk, wred, K + 1, 0);
-          team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
-          LOGIC(after_gradfb<K>(cs, a, s, tid, red));
-        } else {
-          constexpr int NV = WC + WG * (K + 1);
-          const int wlo = cs->gwin_lo;
-          float al[WC];
-          {
-            double v = a.step0;
-#pragma unroll
-            for (int m = 0; m < WC; ++m) {
-              al[m] = (float)v;
-              v *= a.shrink;
-            }
-          }
-          float cst[WC];
-          float pk[WG * (K + 1)];
-#pragma unroll
-          for (int m = 0; m < WC; ++m) cst[m] = 0.f;
-#pragma unroll
-          for (int i = 0; i < WG * (K + 1); ++i) pk[i] = 0.f;
-          for (int slot = 0; slot < nslots; ++slot) {
-            const int qi = slot * TM_NT + tid;
-            float r[4], w[4], ud[4];
-            f4(qi < qcount ? sR[qi] : z4, r);
-            weights(qi, w);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float u[RS];
-              load_row(slot, e, u);
+              rows(e, u);
+              if (WCOL) w[e] = u[RS - 1];
+              r[e] = trial(r[e], pa, udo[e]);  // pending accepted step (exact no-op at 0)
               const float d = dotk<K>(u, sfv[1]);
               ud[e] = d;
-              // trial costs for every window step; the gradient only for the
-              // speculative pair (same arithmetic as penalty_t, split)
-              float ts[WG], hs[WG], es[WG];
-#pragma unroll
-              for (int mm = 0; mm < WG; ++mm) ts[mm] = hs[mm] = es[mm] = 0.f;
+              float gs[WG];
 #pragma unroll
               for (int m = 0; m < WC; ++m) {
                 const float t = trial(r[e], al[m], d);
@@ -490,28 +552,14 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
                   const float h = rsqrtf(b);
                   const float q = rsqrtf(h);
                   cst[m] += q * w[e];
-#pragma unroll
-                  for (int mm = 0; mm < WG; ++mm) {
-                    const bool sel = m == wlo + mm;
-                    ts[mm] = sel ? t : ts[mm];
-                    hs[mm] = sel ? h : hs[mm];
-                    es[mm] = sel ? q : es[mm];
-                  }
+                  if (m >= WLO && m < WLO + WG) gs[m - WLO] = 0.5f * t * (q * w[e]) * (h * h);
                 } else {
                   float tw, g;
                   penalty_t<PM>(t, w[e], a, tw, g);
                   cst[m] += tw;
-#pragma unroll
-                  for (int mm = 0; mm < WG; ++mm) {
-                    const bool sel = m == wlo + mm;
-                    ts[mm] = sel ? g : ts[mm];
-                  }
+                  if (m >= WLO && m < WLO + WG) gs[m - WLO] = g;
                 }
               }
-              float gs[WG];
-#pragma unroll
-              for (int mm = 0; mm < WG; ++mm)
-                gs[mm] = PM == PM_HALF ? 0.5f * ts[mm] * (es[mm] * w[e]) * (hs[mm] * hs[mm]) : ts[mm];
 #pragma unroll
               for (int mm = 0; mm < WG; ++mm) {
                 pk[mm * (K + 1) + K] += gs[mm] * gs[mm];
@@ -519,56 +567,60 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
                 for (int j = 0; j < K; ++j) pk[mm * (K + 1) + j] += u[j] * gs[mm];
               }
             }
-            if (qi < qcount) sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
-          }
-#pragma unroll
-          for (int m = 0; m < WC; ++m) rstage((double)cst[m], wred, m, NV);
-          stage_floats<WG * (K + 1)>(pk, wred, NV, WC);
-          team_sum(ra, team, rank, wred, NV, red, epoch, sprof);
-          LOGIC(after_iter<K>(cs, a, s, tid, red, wlo));
-        }
-        __syncthreads();
-        // apply an accepted step to the residual kept in shared memory
-        const float pa = (float)cs->pend_alpha;
-        if (pa != 0.f) {
-          for (int slot = 0; slot < nslots; ++slot) {
-            const int qi = slot * TM_NT + tid;
-            if (qi >= qcount) continue;
-            float r[4], ud[4];
-            f4(sR[qi], r);
-            f4(sD[qi], ud);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) r[e] = trial(r[e], pa, ud[e]);
             sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
-          }
+            sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
+          });
+        };
+        static_assert(WC - WG <= 4, "window positions");
+        switch (wlo) {
+          case 0: iter_sweep(IC<0>{}); break;
+          case 1: iter_sweep(IC<(1 <= WC - WG ? 1 : 0)>{}); break;
+          case 2: iter_sweep(IC<(2 <= WC - WG ? 2 : 0)>{}); break;
+          case 3: iter_sweep(IC<(3 <= WC - WG ? 3 : 0)>{}); break;
+          default: iter_sweep(IC<(4 <= WC - WG ? 4 : 0)>{}); break;
         }
-        __syncthreads();
-        if (tid == 0) cs->pend_alpha = 0.0;
-        __syncthreads();
+        if (tid == 0) cs->pend_alpha = 0.0;  // consumed by this sweep
+#pragma unroll
+        for (int m = 0; m < WC; ++m) rstage((double)cst[m], wred, m, NV);
+        stage_floats<WG * (K + 1)>(pk, wred, NV, WC);
+        team_sum(ra, team, rank, wred, NV, red, epoch, sprof);
+        LOGIC(after_iter<K>(cs, a, s, tid, red, wlo));
       }
+      __syncthreads();
     }
     PHASE_MARK(PROF_T_ITER);
 
     if (cs->status == ST_OK) {
-      // ---- geodesic step + relabel (manifold.py:116-197, tracker.py:146-147) ---
+      // ---- geodesic step + relabel (manifold.py:116-197, tracker.py:146-147) --
+      // r' = x - U'y = r - coef (v . y), since row i of U' is u_i + coef_i v^T.
       // With a re-orthonormalization due (every 1000th step) U' is written back
-      // unlabeled; the streamed k_gram / k_geo<QR> kernels that follow every
+      // unlabeled; the streamed k_gram / k_geo<QR> kernels that follow the
       // launch apply U' R^-1 and relabel (manifold.py:192-196).
+      if (tid < 32) {
+        const double vj = tid < k ? cs->v[tid] : 0.0, yj = tid < k ? cs->y[tid] : 0.0;
+        const double vy = warp_sum(vj * yj);
+        if (tid == 0) s_vy = (float)vy;
+      }
+      __syncthreads();
       const bool geo = cs->do_geo != 0, qr = geo && cs->qr_now != 0;
       const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s, ln = (float)cs->geo_ln;
+      const float pa = (float)cs->pend_alpha, vy = geo ? s_vy : 0.f;
       float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
-      for (int slot = 0; slot < nslots; ++slot) {
-        const int qi = slot * TM_NT + tid;
+      sweep([&](int qi, const auto& rows) {
         const bool ok = qi < qcount;
         const int pix = (q0 + qi) * 4;
-        float r[4], w[4];
-        f4(ok ? sR[qi] : z4, r);
-        weights(qi, w);
+        float r[4], w[4], ud[4];
+        f4(sR[qi], r);
+        f4(sD[qi], ud);
+        if (!WCOL) lab_weights(qi, w);
         float up[4][K];  // U' rows of this row group
+        float rr[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float u[RS];
-          load_row(slot, e, u);
+          rows(e, u);
+          if (WCOL) w[e] = u[RS - 1];
+          r[e] = trial(r[e], pa, ud[e]);
           float coef = 0.f;
           if (geo) {
             float tw, g;
@@ -580,8 +632,9 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
 #pragma unroll
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
+          rr[e] = fmaf(-coef, vy, r[e]);
         }
-        if (!ok) continue;
+        if (!ok) return;
         if (geo) {
 #pragma unroll
           for (int j = 0; j < K; ++j)
@@ -589,18 +642,12 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
               __stcs(reinterpret_cast<float4*>(Ug + (size_t)j * a.np + pix),
                      make_float4(up[0][j], up[1][j], up[2][j], up[3][j]));
         }
-        if (qr) continue;
-        const size_t off = (size_t)s * a.np + pix;
-        float xh[4], bgn[4], rr[4];
-        f4(sX[qi], xh);
+        if (qr) return;
+        const size_t off = so + pix;
         uint32_t nl = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float acc = dotk<K>(up[e], sfv[0]);
-          bgn[e] = acc;
-          rr[e] = __fsub_rn(xh[e], acc);
-          if (pix + e < a.P && fabs((double)rr[e]) >= a.delta) nl |= 1u << (8 * e);
-        }
+        for (int e = 0; e < 4; ++e)
+          if (pix + e < a.P && fabsf(rr[e]) >= a.delta) nl |= 1u << (8 * e);
         *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
         if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
         if (a.res_out)
@@ -610,17 +657,21 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           float m4[4], b[4];
           f4(a.pipeline ? *reinterpret_cast<const float4*>(Mg + off) : z4, m4);
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
+          for (int e = 0; e < 4; ++e) {
+            const float acc = dotk<K>(up[e], sfv[0]);
+            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(acc * sc, m4[e]), 0.f), 1.f) : acc;
+          }
           *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + off) = make_float4(b[0], b[1], b[2], b[3]);
         }
-      }
+      });
     }
 
     // ---- commit the control block (one writer per stream) ------------------
     __syncthreads();
     PHASE_MARK(PROF_T_GEO);
 #undef PHASE_MARK
+    if (tid == 0) cs->pend_alpha = 0.0;
+    __syncthreads();
     if (rank == 0 && tid < (int)(sizeof(Ctl) / 8))
       reinterpret_cast<double*>(a.ctl + s)[tid] = reinterpret_cast<const double*>(cs)[tid];
     __syncthreads();
@@ -633,7 +684,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tbase), "n"(TM_NT));
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tbase), "n"(TM_NT));
 }
 
 }  // namespace prost
