@@ -46,7 +46,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
     ap.add_argument("--streams", type=int, default=None, help="streams per rank")
-    ap.add_argument("--frames", type=int, default=8, help="distinct frames staged per stream")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="distinct frames staged per stream and cycled (0: every step gets the "
+                         "stream's next consecutive frame, generated on the device)")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--cpu-frames", type=int, default=12, help="oracle frames per CPU worker")
     ap.add_argument("--no-cpu", action="store_true")
@@ -287,10 +289,32 @@ def main():
     k = cfg.subspace_dim
     stream_ids = shard_streams(rank, S)
 
+    preroll = cfg.i_init if args.preroll is None else args.preroll
+    e2e_frames = 0 if args.no_e2e else 2 + args.steps
+    need = preroll + args.warmup + args.steps + 3 + e2e_frames
     t_gen = time.perf_counter()
-    host = gen_frames(args.config, stream_ids, args.frames)  # [F, S, n] float32
+    if args.frames > 0:
+        # a few distinct frames, cycled (numpy generator, bit-identical to the tests' streams)
+        host = gen_frames(args.config, stream_ids, args.frames)  # [F, S, n] float32
+        frames_dev = torch.from_numpy(host).to(f"cuda:{dev}")
+        data_note = (f"synthetic (seeded SURVEY.md §8(d) generator, {args.frames} distinct frames "
+                     "per stream staged in HBM and cycled)")
+    else:
+        # every step is the next consecutive frame of every stream (a cycled
+        # clip would restart the scene every few frames and distort the line
+        # search); the scene model runs on the device
+        from paper_1302_2073_b200.synth import DeviceScenes, config_spec
+
+        scenes = DeviceScenes([config_spec(args.config, sid) for sid in stream_ids], f"cuda:{dev}",
+                              seed=1000 + rank)
+        frames_dev = scenes.next_frames(need)
+        del scenes
+        host = None
+        data_note = (f"synthetic (seeded SURVEY.md §8(d) scene model run on the device: {need} "
+                     "consecutive frames per stream staged in HBM, a new frame every step)")
+    torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
-    frames_dev = torch.from_numpy(host).to(f"cuda:{dev}")
+    F = frames_dev.shape[0]
     bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev)
     if args.wave:
         bt.native.set_wave(args.wave)
@@ -306,9 +330,6 @@ def main():
     mask = torch.empty((S, P), dtype=torch.uint8, device=f"cuda:{dev}")
     bg = torch.empty((S, n), dtype=torch.float32 if args.precision == "fp32" else torch.float64,
                      device=f"cuda:{dev}")
-    if args.precision == "fp64":
-        frames_dev = frames_dev.double()
-    F = args.frames
 
     def barrier():
         if ws > 1:
@@ -320,7 +341,6 @@ def main():
         return reduce_max(v, ws, f"cuda:{dev}")
 
     step = 0
-    preroll = cfg.i_init if args.preroll is None else args.preroll
     torch.cuda.synchronize()
     t_pre = time.perf_counter()
     for _ in range(preroll):
@@ -370,19 +390,26 @@ def main():
     # end to end through the public API: pinned host frames in, host mask + bg out
     e2e = None
     if not args.no_e2e:
-        host_pinned = torch.from_numpy(host).pin_memory()
-        if args.precision == "fp64":
-            host_pinned = host_pinned.double().pin_memory()
+        if host is not None:
+            host_pinned = torch.from_numpy(host).pin_memory()
+            e2e0, HF = 0, host_pinned.shape[0]
+        else:
+            # the e2e frames continue the streams: stage them in pinned host memory
+            e2e0, HF = step, e2e_frames
+            host_pinned = torch.empty((HF,) + tuple(frames_dev.shape[1:]), dtype=frames_dev.dtype,
+                                      pin_memory=True)
+            host_pinned.copy_(frames_dev[e2e0:e2e0 + HF])
+
         mask_h = torch.empty((S, P), dtype=torch.uint8).pin_memory()
         bg_h = torch.empty((S, n), dtype=bg.dtype).pin_memory()
         for _ in range(2):
-            bt.push(host_pinned[step % F], background=bg_h, mask=mask_h)
+            bt.push(host_pinned[(step - e2e0) % HF], background=bg_h, mask=mask_h)
             step += 1
         torch.cuda.synchronize()
         barrier()
         e0.record()
         for _ in range(args.steps):
-            bt.push(host_pinned[step % F], background=bg_h, mask=mask_h)
+            bt.push(host_pinned[(step - e2e0) % HF], background=bg_h, mask=mask_h)
             step += 1
         e1.record()
         torch.cuda.synchronize()
@@ -437,8 +464,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "f64",
-            "data": f"synthetic (seeded SURVEY.md §8(d) generator, {F} distinct frames per stream "
-                    "staged in HBM and cycled)",
+            "data": data_note,
             "config": {"workload": f"{args.config}: {S} streams/GPU x {W}x{H}x{ch}, k={k}, "
                                    f"p={cfg.p}, mu={cfg.mu}, cg_max_iters={cfg.cg_max_iters}",
                        "streams_per_gpu": S, "n": n, "k": k, "precision": args.precision,

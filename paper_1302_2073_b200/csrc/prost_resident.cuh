@@ -32,6 +32,7 @@ struct RArgs {
   int S;            // streams
   unsigned long long* prof;  // [gridDim][8] optional timing counters (ns), or null
   int stagger_ns;            // start delay of odd teams (k_tmem), 0 = none
+  int prefetch;              // k_tmem: L2 prefetch of the next stream's slice
 };
 
 // Timing counters of one CTA (thread 0, %globaltimer ns): see PROF_* below.

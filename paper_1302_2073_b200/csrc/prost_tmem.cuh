@@ -127,6 +127,11 @@ struct SmemRows {
 template <int V>
 using IC = std::integral_constant<int, V>;
 
+// Bulk prefetch of [p, p + bytes) into L2 (no destination, no completion).
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <int K, int PM>
 __global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
@@ -264,6 +269,21 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         }
       }
       tmem_wait_st();
+      // Prefetch this CTA's slice of the team's next stream into L2 so that
+      // its load (and pass 0's frame / mean reads) hit L2 a round from now.
+      if (ra.prefetch && s + T < ra.S && qcount > 0 && tid < k + 3) {
+        const int sn = s + T;
+        const size_t pofs = (size_t)q0 * 4;
+        const unsigned pb = (unsigned)qcount * 16u;
+        if (tid < k)
+          prefetch_l2(static_cast<const float*>(a.U) + ((size_t)sn * k + tid) * a.np + pofs, pb);
+        else if (tid == k)
+          prefetch_l2(Xg + (size_t)sn * a.np + pofs, pb);
+        else if (tid == k + 1 && a.pipeline)
+          prefetch_l2(Mg + (size_t)sn * a.np + pofs, pb);
+        else if (tid == k + 2)
+          prefetch_l2(a.lab + (size_t)sn * a.Pp + pofs, ((unsigned)qcount * 4u + 15u) / 16u * 16u);
+      }
       if (tid < (int)(sizeof(Ctl) / 8))
         reinterpret_cast<double*>(cs)[tid] = __ldcg(reinterpret_cast<const double*>(a.ctl + s) + tid);
       __syncthreads();

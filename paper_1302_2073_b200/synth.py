@@ -182,3 +182,102 @@ def config_spec(name: str, stream: int = 0, **overrides) -> SceneSpec:
     kw.update(overrides)
     kw.setdefault("seed", stream)
     return SceneSpec(**kw)
+
+
+class DeviceScenes:
+    """The same scene model for many streams at once, advanced on a CUDA device
+    (torch) so that benchmarks can stage long runs of consecutive frames in
+    HBM.  Stream s starts from exactly the state `SceneStream(specs[s])` draws
+    (background mean, basis, coefficients, objects); the per-frame random walk
+    and pixel noise then come from a seeded torch generator, so the frames
+    follow the model but are not bit-identical to `SceneStream`'s.  Background
+    jitter (C2) is not supported here.
+    """
+
+    def __init__(self, specs, device, seed: int = 0):
+        import torch
+
+        if any(s.jitter for s in specs):
+            raise ValueError("DeviceScenes does not model background jitter")
+        s0 = specs[0]
+        if any((s.width, s.height, s.channels, s.rank) != (s0.width, s0.height, s0.channels, s0.rank)
+               for s in specs):
+            raise ValueError("all streams must share shape and rank")
+        self.torch = torch
+        self.specs = list(specs)
+        self.dev = torch.device(device)
+        self.gen = torch.Generator(device=self.dev)
+        self.gen.manual_seed(seed)
+        S, C, H, W = len(specs), s0.channels, s0.height, s0.width
+        self.shape = (S, C, H, W)
+        host = [SceneStream(s, dtype=np.float32) for s in specs]
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.mu0 = torch.tensor(np.stack([h._mu0 for h in host]), **f32)            # [S, n]
+        self.basis = torch.tensor(np.stack([h._basis for h in host]), **f32)        # [S, n, r]
+        self.coef = torch.tensor(np.stack([h._coef for h in host]), **f32)          # [S, r]
+        self.amp = torch.tensor([s.amplitude for s in specs], **f32)[:, None]
+        self.walk = torch.tensor([s.walk for s in specs], **f32)[:, None]
+        self.noise = torch.tensor([s.noise for s in specs], **f32)[:, None]
+        self.fg_from = torch.tensor([s.fg_from for s in specs], device=self.dev)
+        nob = max(len(h._objects) for h in host)
+        i32 = dict(dtype=torch.int64, device=self.dev)
+        ob = np.zeros((S, nob, 6), dtype=np.int64)
+        col = np.zeros((S, nob, C), dtype=np.float32)
+        act = np.zeros((S, nob), dtype=bool)
+        for i, h in enumerate(host):
+            for j, o in enumerate(h._objects):
+                ob[i, j] = o[:6]
+                col[i, j] = o[6]
+                act[i, j] = True
+        self.ob = torch.tensor(ob, **i32)      # y0, x0, h, w, vy, vx
+        self.col = torch.tensor(col, **f32)    # [S, nob, C]
+        self.act = torch.tensor(act, device=self.dev)
+        self.ellipse = torch.tensor([s.shape == "ellipse" for s in specs], device=self.dev)
+        self.yy = torch.arange(H, device=self.dev)[None, :, None]
+        self.xx = torch.arange(W, device=self.dev)[None, None, :]
+        self.t = 0
+
+    def _frame(self):
+        torch = self.torch
+        S, C, H, W = self.shape
+        bg = self.mu0 + self.amp * torch.bmm(self.basis, self.coef[:, :, None])[:, :, 0]
+        img = bg.clamp(0.0, 1.0).view(S, C, H, W)
+        paint = self.t >= self.fg_from  # [S]
+        for j in range(self.ob.shape[1]):
+            y0, x0, h, w, vy, vx = (self.ob[:, j, c] for c in range(6))
+            rect = ((self.yy >= y0[:, None, None]) & (self.yy < (y0 + h)[:, None, None]) &
+                    (self.xx >= x0[:, None, None]) & (self.xx < (x0 + w)[:, None, None]))
+            cy = (y0 + (h - 1) / 2.0)[:, None, None]
+            cx = (x0 + (w - 1) / 2.0)[:, None, None]
+            ell = (((self.yy - cy) / (h / 2.0)[:, None, None]) ** 2 +
+                   ((self.xx - cx) / (w / 2.0)[:, None, None]) ** 2) <= 1.0
+            sel = torch.where(self.ellipse[:, None, None], ell, rect)
+            sel = sel & (self.act[:, j] & paint)[:, None, None]
+            img = torch.where(sel[:, None], self.col[:, j, :, None, None], img)
+            # advance with bouncing (SceneStream._paint)
+            ny, nx = y0 + vy, x0 + vx
+            by = (ny < 0) | (ny + h > H)
+            bx = (nx < 0) | (nx + w > W)
+            vy = torch.where(by, -vy, vy)
+            vx = torch.where(bx, -vx, vx)
+            ny = torch.where(by, torch.minimum(torch.clamp(y0 + vy, min=0), H - h), ny)
+            nx = torch.where(bx, torch.minimum(torch.clamp(x0 + vx, min=0), W - w), nx)
+            adv = paint & self.act[:, j]
+            self.ob[:, j, 0] = torch.where(adv, ny, y0)
+            self.ob[:, j, 1] = torch.where(adv, nx, x0)
+            self.ob[:, j, 4] = torch.where(adv, vy, self.ob[:, j, 4])
+            self.ob[:, j, 5] = torch.where(adv, vx, self.ob[:, j, 5])
+        img = img.reshape(S, -1)
+        img = img + self.noise * torch.randn(img.shape, generator=self.gen, device=self.dev)
+        self.coef = self.coef + self.walk * torch.randn(self.coef.shape, generator=self.gen,
+                                                        device=self.dev)
+        self.t += 1
+        return img.clamp_(0.0, 1.0)
+
+    def next_frames(self, count: int):
+        """The next `count` frames of every stream: a float32 [count, S, n] tensor."""
+        S, C, H, W = self.shape
+        out = self.torch.empty((count, S, C * H * W), dtype=self.torch.float32, device=self.dev)
+        for i in range(count):
+            out[i] = self._frame()
+        return out
