@@ -298,7 +298,13 @@ __device__ __forceinline__ double alpha_at(const Args& a, int m) {
 
 static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied as 8-byte words");
 
-__device__ __noinline__ void write_info(Ctl* c, const Args& a, int s) {
+// Linkage of the scalar decision functions below (PROST_LOGIC=__forceinline__
+// inlines them into every kernel).
+#ifndef PROST_LOGIC
+#define PROST_LOGIC __noinline__
+#endif
+
+__device__ PROST_LOGIC void write_info(Ctl* c, const Args& a, int s) {
   if (!a.info || c->no_info) return;
   FitInfo fi;
   fi.fit_cost = c->f;
@@ -313,7 +319,7 @@ __device__ __noinline__ void write_info(Ctl* c, const Args& a, int s) {
 
 // End of the CG loop: projected-gradient norm, geodesic scalars
 // (manifold.py:130-197, tracker.py:140-143).
-__device__ __noinline__ void finish_frame(Ctl* c, const Args& a, int s, int lane) {
+__device__ PROST_LOGIC void finish_frame(Ctl* c, const Args& a, int s, int lane) {
   const double t = step_size(a, c->frame_index);
   const double gj = lane < a.k ? c->grad[lane] : 0.0;  // = U^T eta
   const double yj = lane < a.k ? c->y[lane] : 0.0;
@@ -333,8 +339,10 @@ __device__ __noinline__ void finish_frame(Ctl* c, const Args& a, int s, int lane
     } else {
       const double phi = (ln * rn) * t;
       c->do_geo = 1;
-      c->geo_a = cos(phi) - 1.0;
-      c->geo_s = sin(phi);
+      double sphi, cphi;
+      sincos(phi, &sphi, &cphi);
+      c->geo_a = cphi - 1.0;
+      c->geo_s = sphi;
       c->geo_ln = ln;
       c->since_qr += 1;
       c->qr_now = c->since_qr >= QR_EVERY ? 1 : 0;
@@ -346,7 +354,7 @@ __device__ __noinline__ void finish_frame(Ctl* c, const Args& a, int s, int lane
 }
 
 // Top of CG iteration c->it (fit.py:108-119).
-__device__ __noinline__ void begin_iteration(Ctl* c, const Args& a, int s, int lane) {
+__device__ PROST_LOGIC void begin_iteration(Ctl* c, const Args& a, int s, int lane) {
   if (lane == 0) {
     c->need_lsfb = 0;
     c->need_gradfb = 0;
@@ -379,7 +387,7 @@ __device__ __noinline__ void begin_iteration(Ctl* c, const Args& a, int s, int l
 
 // Accepted step alpha with cost fnew and coordinate-gradient sums gs[j]
 // (= sum_i U_ij g_i): fit.py:137-144.
-__device__ __noinline__ void complete_iteration(Ctl* c, const Args& a, int s, int lane, double alpha,
+__device__ PROST_LOGIC void complete_iteration(Ctl* c, const Args& a, int s, int lane, double alpha,
                                    double fnew, const double* gs, double gsq_new) {
   const double dj = lane < a.k ? c->d[lane] : 0.0;
   const double gold = lane < a.k ? c->grad[lane] : 0.0;
@@ -406,7 +414,7 @@ __device__ __noinline__ void complete_iteration(Ctl* c, const Args& a, int s, in
   begin_iteration(c, a, s, lane);
 }
 
-__device__ __noinline__ void fail_iteration(Ctl* c, const Args& a, int s, int lane) {
+__device__ PROST_LOGIC void fail_iteration(Ctl* c, const Args& a, int s, int lane) {
   // fit.py:133-134: no acceptable step -> leave the loop, residual unchanged
   if (lane == 0) c->pend_alpha = 0.0;
   __syncwarp();
@@ -429,7 +437,7 @@ __device__ __forceinline__ void mark_nonfinite(Ctl* c, const Args& a, int s, int
 
 // red: [0] cost, [1..K] sum_i U_ij g_i, [K+1] ||g||^2, [K+2] non-finite count
 template <int K>
-__device__ __noinline__ void after_pass0(Ctl* c, const Args& a, int s, int lane, const double* red) {
+__device__ PROST_LOGIC void after_pass0(Ctl* c, const Args& a, int s, int lane, const double* red) {
   if (red[K + 2] > 0.0) { mark_nonfinite(c, a, s, lane); return; }
   if (lane < a.k) {
     const double gj = -red[1 + lane];  // fit.py:101: grad = -(U^T g)
@@ -451,7 +459,7 @@ __device__ __noinline__ void after_pass0(Ctl* c, const Args& a, int s, int lane,
 
 // red: [0..WC) trial costs, then per speculative slot mm: K gradient sums + ||g||^2
 template <int K>
-__device__ __noinline__ void after_iter(Ctl* c, const Args& a, int s, int lane, const double* red, int wlo) {
+__device__ PROST_LOGIC void after_iter(Ctl* c, const Args& a, int s, int lane, const double* red, int wlo) {
   const int nmax = a.max_bt < WC ? a.max_bt : WC;
   int first = -1;
   double alpha = a.step0;
@@ -494,7 +502,7 @@ __device__ __noinline__ void after_iter(Ctl* c, const Args& a, int s, int lane, 
 }
 
 // red: [0..cnt) trial costs for step indices base..base+cnt-1
-__device__ __noinline__ void after_lsfb(Ctl* c, const Args& a, int s, int lane, const double* red, int base) {
+__device__ PROST_LOGIC void after_lsfb(Ctl* c, const Args& a, int s, int lane, const double* red, int base) {
   const int cnt = (a.max_bt - base) < LSW ? (a.max_bt - base) : LSW;
   int first = -1;
   double alpha = alpha_at(a, base);
@@ -531,7 +539,7 @@ __device__ __noinline__ void after_lsfb(Ctl* c, const Args& a, int s, int lane, 
 
 // red: [0..K) gradient sums at the accepted step, [K] ||g||^2
 template <int K>
-__device__ __noinline__ void after_gradfb(Ctl* c, const Args& a, int s, int lane, const double* red) {
+__device__ PROST_LOGIC void after_gradfb(Ctl* c, const Args& a, int s, int lane, const double* red) {
   if (lane == 0) c->need_gradfb = 0;
   __syncwarp();
   complete_iteration(c, a, s, lane, c->acc_alpha, c->acc_cost, red, red[K]);

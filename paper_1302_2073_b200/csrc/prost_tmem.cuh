@@ -13,9 +13,8 @@
 // 12 streams are in flight; U crosses HBM exactly once each way per frame.
 //
 // What is kept per row group besides U: the residual r and the last u_dir = U d
-// (shared memory).  The frame itself is re-read from global memory by the one
-// sweep that needs it (pass 0), and the relabel uses r' = r - coef (v . y)
-// (row i of U' is u_i + coef_i v^T), so no copy of the frame is kept on chip.
+// (shared memory).  The frame itself is re-read from global memory (L2) by the
+// two sweeps that need it (pass 0 and the relabel), so no copy is kept on chip.
 // With k < 16 the per-coordinate weight w (1, omega, or 0 for padding) rides in
 // the unused 16th TMEM / shared-memory column of each row.
 //
@@ -142,7 +141,6 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   __shared__ unsigned s_tbase;
   __shared__ unsigned long long sprof[PROF_N];
   __shared__ float sfv[4][K];  // fp32 copies of y, d, v, grad for the per-element math
-  __shared__ float s_vy;       // v . y of the geodesic step (relabel without the frame)
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -210,8 +208,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     for (int slot = 0; slot < nst; ++slot)
       body(slot * TM_NT + tid, TmemRows<RS>{tbase + (unsigned)(slot * QW)});
     for (int slot = QT; slot < nslots; ++slot) {
-      const int i = (slot - QT) * TM_NT + tid;
-      body(slot * TM_NT + tid, SmemRows<RS>{sU + i, qs, i < qs});
+      const int qi = slot * TM_NT + tid;  // rows past qcount were never loaded
+      body(qi, SmemRows<RS>{sU + (qi - QT * TM_NT), qs, qi < qcount});
     }
   };
   const float omega = a.omegaf;
@@ -612,19 +610,12 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 
     if (cs->status == ST_OK) {
       // ---- geodesic step + relabel (manifold.py:116-197, tracker.py:146-147) --
-      // r' = x - U'y = r - coef (v . y), since row i of U' is u_i + coef_i v^T.
       // With a re-orthonormalization due (every 1000th step) U' is written back
       // unlabeled; the streamed k_gram / k_geo<QR> kernels that follow the
       // launch apply U' R^-1 and relabel (manifold.py:192-196).
-      if (tid < 32) {
-        const double vj = tid < k ? cs->v[tid] : 0.0, yj = tid < k ? cs->y[tid] : 0.0;
-        const double vy = warp_sum(vj * yj);
-        if (tid == 0) s_vy = (float)vy;
-      }
-      __syncthreads();
       const bool geo = cs->do_geo != 0, qr = geo && cs->qr_now != 0;
       const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s, ln = (float)cs->geo_ln;
-      const float pa = (float)cs->pend_alpha, vy = geo ? s_vy : 0.f;
+      const float pa = (float)cs->pend_alpha;
       float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
       sweep([&](int qi, const auto& rows) {
         const bool ok = qi < qcount;
@@ -652,7 +643,6 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
 #pragma unroll
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
-          rr[e] = fmaf(-coef, vy, r[e]);
         }
         if (!ok) return;
         if (geo) {
@@ -664,10 +654,17 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         }
         if (qr) return;
         const size_t off = so + pix;
+        // r' = x - U'y from the frame (tracker.py:146), as the reference orders it
+        float xh[4], bgn[4];
+        bool bad_unused = false;
+        xhat(qi, false, xh, bad_unused);
         uint32_t nl = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int e = 0; e < 4; ++e) {
+          bgn[e] = dotk<K>(up[e], sfv[0]);
+          rr[e] = __fsub_rn(xh[e], bgn[e]);
           if (pix + e < a.P && fabsf(rr[e]) >= a.delta) nl |= 1u << (8 * e);
+        }
         *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
         if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
         if (a.res_out)
@@ -677,10 +674,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           float m4[4], b[4];
           f4(a.pipeline ? *reinterpret_cast<const float4*>(Mg + off) : z4, m4);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float acc = dotk<K>(up[e], sfv[0]);
-            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(acc * sc, m4[e]), 0.f), 1.f) : acc;
-          }
+          for (int e = 0; e < 4; ++e)
+            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
           *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + off) = make_float4(b[0], b[1], b[2], b[3]);
         }
       });
