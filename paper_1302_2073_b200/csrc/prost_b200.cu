@@ -1062,15 +1062,21 @@ int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n) {
   const int ctas = h->rT * h->rG;
   std::vector<unsigned long long> v((size_t)ctas * PROF_N);
   CK(cudaMemcpy(v.data(), h->rprof, v.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  // per-CTA means of the counters of the last profiled launch, then the max total
-  for (int c = 0; c < ctas; ++c)
-    for (int i = 0; i < PROF_N && i < n; ++i) out[i] += (int64_t)v[(size_t)c * PROF_N + i];
-  for (int i = 0; i < PROF_N && i < n; ++i) out[i] /= ctas;
-  if (n >= PROF_N) {
-    unsigned long long mx = 0;
-    for (int c = 0; c < ctas; ++c) mx = std::max(mx, v[(size_t)c * PROF_N]);
-    out[PROF_N - 1] = (int64_t)mx;
+  // per-CTA means of the counters of the last profiled launch (time counters
+  // converted from SM clocks to ns with the CTA's own clock rate), then the
+  // max kernel time
+  const bool is_time[PROF_N] = {true, true, true, true, true, false, false,
+                                true, true, true, true, false};
+  std::vector<double> acc(PROF_N, 0.0);
+  unsigned long long mx = 0;
+  for (int c = 0; c < ctas; ++c) {
+    const unsigned long long* cv = v.data() + (size_t)c * PROF_N;
+    const double ns_per_clk = cv[PROF_TOTAL] ? (double)cv[PROF_GT_TOTAL] / (double)cv[PROF_TOTAL] : 0.0;
+    for (int i = 0; i < PROF_N; ++i) acc[i] += is_time[i] ? cv[i] * ns_per_clk : (double)cv[i];
+    mx = std::max(mx, cv[PROF_GT_TOTAL]);
   }
+  for (int i = 0; i < PROF_N && i < n; ++i) out[i] = (int64_t)(acc[i] / ctas);
+  if (n >= PROF_N) out[PROF_N - 1] = (int64_t)mx;
   return PROST_OK;
 }
 

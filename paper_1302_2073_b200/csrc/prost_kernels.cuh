@@ -301,7 +301,7 @@ static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied as 8-byte words");
 // Linkage of the scalar decision functions below (PROST_LOGIC=__forceinline__
 // inlines them into every kernel).
 #ifndef PROST_LOGIC
-#define PROST_LOGIC __noinline__
+#define PROST_LOGIC __forceinline__
 #endif
 
 __device__ PROST_LOGIC void write_info(Ctl* c, const Args& a, int s) {

@@ -39,8 +39,13 @@ struct RArgs {
 enum {
   PROF_TOTAL = 0, PROF_BARRIER, PROF_SLOTS, PROF_LOGIC, PROF_PREFETCH, PROF_NSUMS, PROF_ROUNDS,
   PROF_T_STATS, PROF_T_PASS0, PROF_T_ITER, PROF_T_GEO,  // phase wall times (k_tmem)
+  PROF_GT_TOTAL,  // kernel time in %globaltimer ns (the others count SM clocks)
   PROF_N = 16
 };
+
+// Profiling clock: SM cycles (the ~1 us tick of %globaltimer is too coarse for
+// sub-microsecond phases); the host converts with PROF_TOTAL / PROF_GT_TOTAL.
+__device__ __forceinline__ unsigned long long ptimer() { return clock64(); }
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -123,7 +128,7 @@ __device__ __forceinline__ void team_sum(const RArgs& ra, int team, int rank, co
                                          unsigned long long* sprof) {
   __syncthreads();
   const bool tp = ra.prof && threadIdx.x == 0;
-  unsigned long long t0 = tp ? gtimer() : 0;
+  unsigned long long t0 = tp ? ptimer() : 0;
   const int nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = ra.G;
   const int par = epoch & 1;
@@ -135,7 +140,7 @@ __device__ __forceinline__ void team_sum(const RArgs& ra, int team, int rank, co
   }
   ++epoch;
   team_barrier(ra.bar + team, epoch * (unsigned)G);
-  unsigned long long t1 = tp ? gtimer() : 0;
+  unsigned long long t1 = tp ? ptimer() : 0;
   for (int v0 = warp; v0 < nv; v0 += 4 * nwarp) {
     double acc[4];
 #pragma unroll
@@ -158,7 +163,7 @@ __device__ __forceinline__ void team_sum(const RArgs& ra, int team, int rank, co
   }
   __syncthreads();
   if (tp) {
-    const unsigned long long t2 = gtimer();
+    const unsigned long long t2 = ptimer();
     sprof[PROF_BARRIER] += t1 - t0;
     sprof[PROF_SLOTS] += t2 - t1;
     sprof[PROF_NSUMS] += 1;
@@ -248,12 +253,12 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ A
   unsigned epoch = 0;
   __shared__ unsigned long long sprof[PROF_N];
   if (tid < PROF_N) sprof[tid] = 0;
-  const unsigned long long t_start = gtimer();
+  const unsigned long long t_start = ptimer(), g_start = gtimer();
 #define LOGIC(call)                                                    \
   do {                                                                 \
-    const unsigned long long tl0 = (ra.prof && tid == 0) ? gtimer() : 0; \
+    const unsigned long long tl0 = (ra.prof && tid == 0) ? ptimer() : 0; \
     if (tid < 32) call;                                                \
-    if (ra.prof && tid == 0) sprof[PROF_LOGIC] += gtimer() - tl0;      \
+    if (ra.prof && tid == 0) sprof[PROF_LOGIC] += ptimer() - tl0;      \
   } while (0)
 
   if (tid == 0) mbar_init(mbar, 1);
@@ -275,10 +280,10 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ A
   for (int s = team; s < ra.S; s += T, ++round) {
     // ---- stage the prefetched slice into registers -------------------------
     {
-      const unsigned long long tw0 = (ra.prof && tid == 0) ? gtimer() : 0;
+      const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
       if (qcount > 0) mbar_wait(mbar, round & 1);
       if (ra.prof && tid == 0) {
-        sprof[PROF_PREFETCH] += gtimer() - tw0;
+        sprof[PROF_PREFETCH] += ptimer() - tw0;
         sprof[PROF_ROUNDS] += 1;
       }
     }
@@ -673,7 +678,8 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ A
     __syncthreads();
   }
   if (ra.prof && tid == 0) {
-    sprof[PROF_TOTAL] = gtimer() - t_start;
+    sprof[PROF_TOTAL] = ptimer() - t_start;
+    sprof[PROF_GT_TOTAL] = gtimer() - g_start;
     for (int i = 0; i < PROF_N; ++i) ra.prof[(size_t)blockIdx.x * PROF_N + i] = sprof[i];
   }
 #undef LOGIC

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   const float* Xg = static_cast<const float*>(a.x);
 
   if (tid < PROF_N) sprof[tid] = 0;
-  const unsigned long long t_start = gtimer();
+  const unsigned long long t_start = ptimer(), g_start = gtimer();
   // TMEM: TM_NT columns, allocated by warp 0
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -193,13 +193,13 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   } while (0)
 #define LOGIC(call)                                                        \
   do {                                                                     \
-    const unsigned long long tl0 = (ra.prof && tid == 0) ? gtimer() : 0;   \
+    const unsigned long long tl0 = (ra.prof && tid == 0) ? ptimer() : 0;   \
     if (tid < 32) {                                                        \
       call;                                                                \
       __syncwarp();                                                        \
       SYNC_FLOATS();                                                       \
     }                                                                      \
-    if (ra.prof && tid == 0) sprof[PROF_LOGIC] += gtimer() - tl0;          \
+    if (ra.prof && tid == 0) sprof[PROF_LOGIC] += ptimer() - tl0;          \
   } while (0)
 
   // Visit every row group of this thread: body(qi, rows).  TMEM row groups
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     const size_t so = (size_t)s * a.np;  // this stream's plane offset
     // ---- load this stream's slice: U (+ weights) -> TMEM / shared memory ----
     {
-      const unsigned long long tw0 = (ra.prof && tid == 0) ? gtimer() : 0;
+      const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
       const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
       for (int slot = 0; slot < nslots; ++slot) {
         const int qi = slot * TM_NT + tid;  // row group within the slice
@@ -288,14 +288,14 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       if (tid == 0) cs->no_info = rank != 0;
       SYNC_FLOATS();
       __syncthreads();
-      if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += gtimer() - tw0;
+      if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += ptimer() - tw0;
     }
 
-    unsigned long long tph = (ra.prof && tid == 0) ? gtimer() : 0;
+    unsigned long long tph = (ra.prof && tid == 0) ? ptimer() : 0;
 #define PHASE_MARK(idx)                              \
   do {                                               \
     if (ra.prof && tid == 0) {                       \
-      const unsigned long long tn = gtimer();        \
+      const unsigned long long tn = ptimer();        \
       sprof[idx] += tn - tph;                        \
       tph = tn;                                      \
     }                                                \
@@ -694,7 +694,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #undef LOGIC
 #undef SYNC_FLOATS
   if (ra.prof && tid == 0) {
-    sprof[PROF_TOTAL] = gtimer() - t_start;
+    sprof[PROF_TOTAL] = ptimer() - t_start;
+    sprof[PROF_GT_TOTAL] = gtimer() - g_start;
     for (int i = 0; i < PROF_N; ++i) ra.prof[(size_t)blockIdx.x * PROF_N + i] = sprof[i];
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
