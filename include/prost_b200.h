@@ -178,6 +178,34 @@ int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n
 /* Tuning knob: streams per launch wave (0 = automatic, sized to L2). */
 int prost_set_wave(prost_handle* h, int32_t streams_per_wave);
 
+/* ---- Exchange (pixel-sharded) mode, SURVEY.md §8(e) ------------------------
+ * One stream too large for one GPU (BASELINE config C4) is split by image
+ * rows: rank g's handle is created for its block of rows (params.height =
+ * local rows) and switched to exchange mode with the stream's global
+ * coordinate count.  A frame then runs as a phase program; after each phase
+ * with a reduction the caller sums the exchange buffer over ranks (NCCL
+ * all-reduce, in place, on the same CUDA stream) and lets the phase's scalar
+ * logic run — identically on every rank, so the basis row blocks stay one
+ * basis.  The 3x3 median needs the label row above and below the block from
+ * the neighbouring ranks (prost_xedges / prost_xfinish).  Replaces, for one
+ * sharded stream, the same reference seam as prost_push
+ * (StreamTracker.push, jobs.py:186-229, over process_frame, tracker.py:121-156):
+ *
+ *   prost_xbegin(frame)
+ *   while (prost_xnext(&x), x) { allreduce_sum(xred, count); prost_xapply(); }
+ *   prost_xedges(top, bottom); exchange rows with the neighbours
+ *   prost_xfinish(row above or NULL at the image top, row below or NULL)
+ */
+int prost_set_exchange(prost_handle* h, int64_t n_real_global);
+int prost_xbuffer(prost_handle* h, double** xred, int64_t* count);  /* device, [S][nvmax] f64 */
+int prost_xbegin(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
+                 const prost_outputs* out, void* cuda_stream);
+int prost_xnext(prost_handle* h, int32_t* exchange, void* cuda_stream);
+int prost_xapply(prost_handle* h, void* cuda_stream);
+int prost_xedges(prost_handle* h, uint8_t* top, uint8_t* bottom, void* cuda_stream);  /* [S][width] */
+int prost_xfinish(prost_handle* h, const uint8_t* halo_top, const uint8_t* halo_bottom,
+                  void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

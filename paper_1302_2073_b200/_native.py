@@ -28,6 +28,8 @@ EXPORTS = (
     "prost_get_core_state", "prost_set_preproc", "prost_get_preproc", "prost_push",
     "prost_background", "prost_synchronize", "prost_last_error", "prost_query",
     "prost_set_wave", "prost_profile", "prost_profile_read", "prost_resident_counters",
+    "prost_set_exchange", "prost_xbuffer", "prost_xbegin", "prost_xnext", "prost_xapply",
+    "prost_xedges", "prost_xfinish",
 )
 PHASES = ("stats", "cold", "pass0", "iter", "lsfb", "gradfb", "geo", "qr", "median", "frame")
 
@@ -104,6 +106,13 @@ def lib() -> ctypes.CDLL:
     L.prost_profile.argtypes = [vp, i32]
     L.prost_profile_read.argtypes = [vp, dp, ctypes.POINTER(i64), i32]
     L.prost_resident_counters.argtypes = [vp, ctypes.POINTER(i64), i32]
+    L.prost_set_exchange.argtypes = [vp, i64]
+    L.prost_xbuffer.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.prost_xbegin.argtypes = [vp, vp, i32, i32, ctypes.POINTER(Outputs), vp]
+    L.prost_xnext.argtypes = [vp, ctypes.POINTER(i32), vp]
+    L.prost_xapply.argtypes = [vp, vp]
+    L.prost_xedges.argtypes = [vp, vp, vp, vp]
+    L.prost_xfinish.argtypes = [vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("prost_destroy",):
             getattr(L, name).restype = ctypes.c_int

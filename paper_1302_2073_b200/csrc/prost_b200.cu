@@ -32,6 +32,9 @@ struct Ops {
   void (*frame)(prost_handle*, Args&, cudaStream_t, int sw);
   void (*background)(prost_handle*, Args&, cudaStream_t, int sw);
   void (*qr)(prost_handle*, Args&, cudaStream_t, int sw);  // periodic QR pair only
+  // exchange (pixel-sharded) mode: one phase kernel / the logic of a phase
+  void (*step)(prost_handle*, Args&, cudaStream_t, int sw, int xs);
+  void (*xlogic)(prost_handle*, Args&, cudaStream_t, int sw, int xs);
   int K, VEC;
 };
 
@@ -82,6 +85,18 @@ struct prost_handle {
   // periodic re-orthonormalization kernels are launched only when it can be due
   long long qr_bound = 0;
   bool qr_due = true;
+  // exchange (pixel-sharded) mode: prost_xbegin / xnext / xapply / xfinish
+  bool xmode = false;
+  double* xred = nullptr;  // [S][nvmax] partial sums, summed over ranks by the caller
+  int* xgo = nullptr;      // [S]
+  long long n_real_glob = 0;
+  long long frames_pushed = 0;
+  std::vector<int> xprog;  // phase program of the frame in flight
+  size_t xpc = 0;
+  int xlast = -1;          // phase whose partials are in xred
+  Args xa;
+  prost_outputs xo{};
+  bool xactive = false;
   // optional per-phase timing (prost_profile)
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -146,7 +161,11 @@ Args make_args(prost_handle* h, int s0) {
   a.i_init = h->prm.i_init;
   const double p = h->prm.p;
   a.pmode = p == 2.0 ? PM_TWO : (p == 1.0 ? PM_ONE : ((p == 0.5 && !h->fp64) ? PM_HALF : PM_GENERAL));
-  a.n_real = h->C * h->P;
+  a.n_real = h->xmode ? h->n_real_glob : (long long)h->C * h->P;
+  if (h->xmode) {
+    a.xred = h->xred;
+    a.xgo = h->xgo;
+  }
   a.p = p;
   a.half_p = 0.5 * p;
   a.mu = h->prm.mu;
@@ -251,6 +270,29 @@ struct Impl {
 
   static void background(prost_handle* h, Args& a, cudaStream_t st, int sw) {
     k_background<T, K, VEC><<<dim3(h->chunks, sw), NT, 0, st>>>(a);
+    h->launches += 1;
+  }
+
+  static void step(prost_handle* h, Args& a, cudaStream_t st, int sw, int xs) {
+    const dim3 grid(h->chunks, sw);
+    long long n = 0;
+    switch (xs) {
+      case XS_STATS: LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_COLD: LAUNCH(PROST_PH_COLD, (k_cold<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_PASS0: LAUNCH(PROST_PH_PASS0, (k_pass0<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_ITER: LAUNCH(PROST_PH_ITER, (k_iter<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_LSFB: LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_GRADFB: LAUNCH(PROST_PH_GRADFB, (k_gradfb<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_GEO: LAUNCH(PROST_PH_GEO, (k_geo<T, K, VEC, false><<<grid, NT, 0, st>>>(a))); break;
+      case XS_GRAM: LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_GEOQR: LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a))); break;
+      default: break;
+    }
+    h->launches += n;
+  }
+
+  static void xlogic(prost_handle* h, Args& a, cudaStream_t st, int sw, int xs) {
+    k_xlogic<K><<<sw, 32, 0, st>>>(a, xs);
     h->launches += 1;
   }
 };
@@ -362,7 +404,8 @@ template <typename T>
 Ops pick(int k) {
 #define PROST_K(KK) \
   if (k <= KK) \
-    return Ops{&Impl<T, KK>::frame, &Impl<T, KK>::background, &Impl<T, KK>::qr, KK, Impl<T, KK>::VEC};
+    return Ops{&Impl<T, KK>::frame, &Impl<T, KK>::background, &Impl<T, KK>::qr, &Impl<T, KK>::step, \
+               &Impl<T, KK>::xlogic, KK, Impl<T, KK>::VEC};
   PROST_K(4)
   PROST_K(8)
   PROST_K(15)
@@ -371,7 +414,7 @@ Ops pick(int k) {
   PROST_K(30)
   PROST_K(32)
 #undef PROST_K
-  return Ops{nullptr, nullptr, nullptr, 0, 0};
+  return Ops{nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0};
 }
 
 int validate(prost_handle* h, const prost_params* p, int n_streams) {
@@ -512,6 +555,104 @@ void rows_to_planes(const double* U, int n_rows_dense, int k, int C, int P, int 
 }
 
 }  // namespace
+
+// prost_push, first half: validation, QR due-check, frame upload, output
+// routing.  Fills *ap / *op for the kernels and push_outputs.
+int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
+               const prost_outputs* out, cudaStream_t st, Args* ap, prost_outputs* op) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!frames) return fail(h, PROST_ERR_DIMENSION, "frames is NULL");
+  if (dtype != PROST_F32 && dtype != PROST_F64 && dtype != PROST_U8)
+    return fail(h, PROST_ERR_CONFIG, "unknown frame dtype %d", dtype);
+  CK(cudaSetDevice(h->device));
+  // A QR is due in this push only for a stream whose steps-since-QR is already
+  // QR_EVERY - 1 (manifold.py:192).  Near that bound, refresh it from the
+  // device (one small synchronous read every ~QR_EVERY frames).
+  if (h->qr_bound >= QR_EVERY - 1) {
+    std::vector<Ctl> cs(h->S);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(cs.data(), h->ctl, (size_t)h->S * sizeof(Ctl), cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (const Ctl& c : cs) mx = std::max(mx, c.since_qr);
+    h->qr_bound = mx;
+  }
+  h->qr_due = h->qr_bound >= QR_EVERY - 1;
+  h->qr_bound += 1;
+  const bool same = (dtype == PROST_F64) == h->fp64 && dtype != PROST_U8;
+  const bool dense = h->P == h->Pp;
+  const void* xdev = h->x;
+  if (on_device && same && dense) {
+    xdev = frames;  // zero-copy: kernels read the caller's device frames
+  } else {
+    int rc = upload_dense(h, frames, dtype, on_device, h->x, h->S * h->C, st);
+    if (rc) return rc;
+  }
+  prost_outputs o{};
+  if (out) o = *out;
+  const int odt = o.dtype == PROST_F64 ? PROST_F64 : PROST_F32;
+  const bool osame = (odt == PROST_F64) == h->fp64;
+  const size_t fbytes = (size_t)h->S * h->np * h->esz;
+  cudaError_t e = cudaSuccess;
+  Args a = make_args(h, 0);
+  a.x = xdev;
+  if (o.background) {
+    if (o.on_device && osame && dense) a.bg_out = o.background;
+    else {
+      if (!h->bgbuf) h->bgbuf = dev_alloc(fbytes, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "bg buffer: %s", cudaGetErrorString(e));
+      a.bg_out = h->bgbuf;
+    }
+  }
+  if (o.residual) {
+    if (o.on_device && osame && dense) a.res_out = o.residual;
+    else {
+      if (!h->resbuf) h->resbuf = dev_alloc(fbytes, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "residual buffer: %s", cudaGetErrorString(e));
+      a.res_out = h->resbuf;
+    }
+  }
+  if (o.mask) {
+    if (o.on_device && dense) a.mask_out = o.mask;
+    else {
+      if (!h->maskbuf) h->maskbuf = (uint8_t*)dev_alloc((size_t)h->S * h->Pp, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "mask buffer: %s", cudaGetErrorString(e));
+      a.mask_out = h->maskbuf;
+    }
+  }
+  if (o.raw_mask && o.on_device && dense) a.raw_out = o.raw_mask;
+  *ap = a;
+  *op = o;
+  return PROST_OK;
+}
+
+// prost_push, second half: outputs the kernels could not write in place, and
+// the FitInfo readback (raises NonFiniteError for a rejected frame).
+int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStream_t st) {
+  const int odt = o.dtype == PROST_F64 ? PROST_F64 : PROST_F32;
+  CK(cudaGetLastError());
+  h->maybe_cold = false;
+  // outputs the kernels could not write in place
+  int rc = PROST_OK;
+  if (o.background && a.bg_out == h->bgbuf)
+    rc = download_dense(h, h->bgbuf, o.background, odt, o.on_device, h->S * h->C, st);
+  if (!rc && o.residual && a.res_out == h->resbuf)
+    rc = download_dense(h, h->resbuf, o.residual, odt, o.on_device, h->S * h->C, st);
+  if (!rc && o.mask && a.mask_out == h->maskbuf) rc = copy_labels(h, h->maskbuf, o.mask, o.on_device, st);
+  if (!rc && o.raw_mask && a.raw_out == nullptr) rc = copy_labels(h, h->lab, o.raw_mask, o.on_device, st);
+  if (rc) return rc;
+  if (o.fit) {
+    CK(cudaMemcpyAsync(h->info_h, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(o.fit, h->info_h, (size_t)h->S * sizeof(FitInfo));
+    int first_bad = PROST_OK;
+    for (int s = 0; s < h->S; ++s) {
+      if (h->info_h[s].status != PROST_OK && first_bad == PROST_OK) first_bad = h->info_h[s].status;
+      if (h->info_h[s].status != PROST_OK && h->info_h[s].frame_index == 0) h->maybe_cold = true;
+    }
+    if (first_bad != PROST_OK) return fail(h, first_bad, "frame contains non-finite values");
+  }
+  return PROST_OK;
+}
 
 // ===========================================================================
 // C ABI
@@ -704,7 +845,7 @@ void prost_destroy(prost_handle* h) {
   if (!h) return;
   void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
                   h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage,
-                  h->rbar, h->rpart, h->rprof};
+                  h->rbar, h->rpart, h->rprof, h->xred, h->xgo};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->info_h) cudaFreeHost(h->info_h);
@@ -846,66 +987,12 @@ int prost_get_preproc(prost_handle* h, int32_t stream, double* mean, double* sc)
 int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
                const prost_outputs* out, void* cuda_stream) {
   if (!h) return PROST_ERR_CONFIG;
-  if (!frames) return fail(h, PROST_ERR_DIMENSION, "frames is NULL");
-  if (dtype != PROST_F32 && dtype != PROST_F64 && dtype != PROST_U8)
-    return fail(h, PROST_ERR_CONFIG, "unknown frame dtype %d", dtype);
-  CK(cudaSetDevice(h->device));
+  if (h->xmode) return fail(h, PROST_ERR_CONFIG, "exchange-mode handle: use prost_xbegin");
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  // A QR is due in this push only for a stream whose steps-since-QR is already
-  // QR_EVERY - 1 (manifold.py:192).  Near that bound, refresh it from the
-  // device (one small synchronous read every ~QR_EVERY frames).
-  if (h->qr_bound >= QR_EVERY - 1) {
-    std::vector<Ctl> cs(h->S);
-    CK(cudaStreamSynchronize(st));
-    CK(cudaMemcpy(cs.data(), h->ctl, (size_t)h->S * sizeof(Ctl), cudaMemcpyDeviceToHost));
-    long long mx = 0;
-    for (const Ctl& c : cs) mx = std::max(mx, c.since_qr);
-    h->qr_bound = mx;
-  }
-  h->qr_due = h->qr_bound >= QR_EVERY - 1;
-  h->qr_bound += 1;
-  const bool same = (dtype == PROST_F64) == h->fp64 && dtype != PROST_U8;
-  const bool dense = h->P == h->Pp;
-  const void* xdev = h->x;
-  if (on_device && same && dense) {
-    xdev = frames;  // zero-copy: kernels read the caller's device frames
-  } else {
-    int rc = upload_dense(h, frames, dtype, on_device, h->x, h->S * h->C, st);
-    if (rc) return rc;
-  }
+  Args a;
   prost_outputs o{};
-  if (out) o = *out;
-  const int odt = o.dtype == PROST_F64 ? PROST_F64 : PROST_F32;
-  const bool osame = (odt == PROST_F64) == h->fp64;
-  const size_t fbytes = (size_t)h->S * h->np * h->esz;
-  cudaError_t e = cudaSuccess;
-  Args a = make_args(h, 0);
-  a.x = xdev;
-  if (o.background) {
-    if (o.on_device && osame && dense) a.bg_out = o.background;
-    else {
-      if (!h->bgbuf) h->bgbuf = dev_alloc(fbytes, &e);
-      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "bg buffer: %s", cudaGetErrorString(e));
-      a.bg_out = h->bgbuf;
-    }
-  }
-  if (o.residual) {
-    if (o.on_device && osame && dense) a.res_out = o.residual;
-    else {
-      if (!h->resbuf) h->resbuf = dev_alloc(fbytes, &e);
-      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "residual buffer: %s", cudaGetErrorString(e));
-      a.res_out = h->resbuf;
-    }
-  }
-  if (o.mask) {
-    if (o.on_device && dense) a.mask_out = o.mask;
-    else {
-      if (!h->maskbuf) h->maskbuf = (uint8_t*)dev_alloc((size_t)h->S * h->Pp, &e);
-      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "mask buffer: %s", cudaGetErrorString(e));
-      a.mask_out = h->maskbuf;
-    }
-  }
-  if (o.raw_mask && o.on_device && dense) a.raw_out = o.raw_mask;
+  int rc0 = push_setup(h, frames, dtype, on_device, out, st, &a, &o);
+  if (rc0) return rc0;
   if (h->resident || h->tmem) {
     // one cooperative launch for the whole frame of every stream, then the median
     const char* stg = getenv("PROST_STAGGER_NS");
@@ -936,29 +1023,134 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
       h->ops.frame(h, a, st, std::min(wave, h->S - s0));
     }
   }
-  CK(cudaGetLastError());
-  h->maybe_cold = false;
-  // outputs the kernels could not write in place
-  int rc = PROST_OK;
-  if (o.background && a.bg_out == h->bgbuf)
-    rc = download_dense(h, h->bgbuf, o.background, odt, o.on_device, h->S * h->C, st);
-  if (!rc && o.residual && a.res_out == h->resbuf)
-    rc = download_dense(h, h->resbuf, o.residual, odt, o.on_device, h->S * h->C, st);
-  if (!rc && o.mask && a.mask_out == h->maskbuf) rc = copy_labels(h, h->maskbuf, o.mask, o.on_device, st);
-  if (!rc && o.raw_mask && a.raw_out == nullptr) rc = copy_labels(h, h->lab, o.raw_mask, o.on_device, st);
+  return push_outputs(h, a, o, st);
+}
+
+// ---------------------------------------------------------------------------
+// Exchange (pixel-sharded) mode: every rank holds a block of
+// image rows of the same stream(s); after each phase kernel the caller sums
+// the partials in the exchange buffer over ranks (NCCL all-reduce), then the
+// phase's scalar logic runs identically on every rank.
+
+int prost_set_exchange(prost_handle* h, int64_t n_real_global) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (n_real_global < (int64_t)h->C * h->P)
+    return fail(h, PROST_ERR_DIMENSION, "global coordinate count %lld is below the local %lld",
+                (long long)n_real_global, (long long)h->C * h->P);
+  CK(cudaSetDevice(h->device));
+  if (!h->xred) {
+    cudaError_t e = cudaSuccess;
+    h->xred = (double*)dev_alloc((size_t)h->S * h->nvmax * sizeof(double), &e);
+    if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "exchange buffer: %s", cudaGetErrorString(e));
+    h->xgo = (int*)dev_alloc((size_t)h->S * sizeof(int), &e);
+    if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "exchange flags: %s", cudaGetErrorString(e));
+  }
+  h->xmode = true;
+  h->tmem = false;  // the phase-kernel (streamed) path is the one with exchange points
+  h->resident = false;
+  h->n_real_glob = n_real_global;
+  return PROST_OK;
+}
+
+int prost_xbuffer(prost_handle* h, double** xred, int64_t* count) {
+  if (!h || !xred || !count) return PROST_ERR_CONFIG;
+  if (!h->xmode) return fail(h, PROST_ERR_CONFIG, "not an exchange-mode handle");
+  *xred = h->xred;
+  *count = (int64_t)h->S * h->nvmax;
+  return PROST_OK;
+}
+
+int prost_xbegin(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
+                 const prost_outputs* out, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!h->xmode) return fail(h, PROST_ERR_CONFIG, "not an exchange-mode handle");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int rc = push_setup(h, frames, dtype, on_device, out, st, &h->xa, &h->xo);
   if (rc) return rc;
-  if (o.fit) {
-    CK(cudaMemcpyAsync(h->info_h, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    std::memcpy(o.fit, h->info_h, (size_t)h->S * sizeof(FitInfo));
-    int first_bad = PROST_OK;
-    for (int s = 0; s < h->S; ++s) {
-      if (h->info_h[s].status != PROST_OK && first_bad == PROST_OK) first_bad = h->info_h[s].status;
-      if (h->info_h[s].status != PROST_OK && h->info_h[s].frame_index == 0) h->maybe_cold = true;
+  std::vector<int>& pg = h->xprog;
+  pg.clear();
+  if (h->pipeline) pg.push_back(XS_STATS);
+  if (h->maybe_cold) pg.push_back(XS_COLD);
+  pg.push_back(XS_PASS0);
+  for (int it = 0; it < h->prm.cg_max_iters; ++it) {
+    pg.push_back(XS_ITER);
+    for (int l = 0; l < h->n_ls; ++l) pg.push_back(XS_LSFB);
+    pg.push_back(XS_GRADFB);
+  }
+  pg.push_back(XS_GEO);
+  if (h->qr_due) {
+    pg.push_back(XS_GRAM);
+    pg.push_back(XS_GEOQR);
+  }
+  h->xpc = 0;
+  h->xlast = -1;
+  h->xactive = true;
+  return PROST_OK;
+}
+
+int prost_xnext(prost_handle* h, int32_t* exchange, void* cuda_stream) {
+  if (!h || !exchange) return PROST_ERR_CONFIG;
+  if (!h->xactive) return fail(h, PROST_ERR_SEQUENCE, "no frame in flight (prost_xbegin)");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  *exchange = 0;
+  while (h->xpc < h->xprog.size()) {
+    const int xs = h->xprog[h->xpc++];
+    h->ops.step(h, h->xa, st, h->S, xs);
+    CK(cudaGetLastError());
+    if (xs != XS_GEO && xs != XS_GEOQR) {
+      h->xlast = xs;
+      *exchange = 1;
+      return PROST_OK;
     }
-    if (first_bad != PROST_OK) return fail(h, first_bad, "frame contains non-finite values");
   }
   return PROST_OK;
+}
+
+int prost_xapply(prost_handle* h, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!h->xactive || h->xlast < 0) return fail(h, PROST_ERR_SEQUENCE, "no exchange pending");
+  CK(cudaSetDevice(h->device));
+  h->ops.xlogic(h, h->xa, (cudaStream_t)cuda_stream, h->S, h->xlast);
+  h->xlast = -1;
+  CK(cudaGetLastError());
+  return PROST_OK;
+}
+
+int prost_xedges(prost_handle* h, uint8_t* top, uint8_t* bottom, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int W = h->prm.width, H = h->prm.height;
+  if (top) CK(cudaMemcpy2DAsync(top, W, h->lab, h->Pp, W, h->S, cudaMemcpyDeviceToDevice, st));
+  if (bottom)
+    CK(cudaMemcpy2DAsync(bottom, W, h->lab + (size_t)(H - 1) * W, h->Pp, W, h->S,
+                         cudaMemcpyDeviceToDevice, st));
+  return PROST_OK;
+}
+
+int prost_xfinish(prost_handle* h, const uint8_t* halo_top, const uint8_t* halo_bottom,
+                  void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!h->xactive || h->xpc < h->xprog.size() || h->xlast >= 0)
+    return fail(h, PROST_ERR_SEQUENCE, "frame program not finished");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  h->xactive = false;
+  Args a = h->xa;
+  a.halo_top = halo_top;
+  a.halo_bot = halo_bottom;
+  if (a.mask_out) {
+    if (h->prm.width % 4 != 0 || ((uintptr_t)a.mask_out & 3) || ((uintptr_t)halo_top & 3) ||
+        ((uintptr_t)halo_bottom & 3)) {
+      const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), h->S);
+      k_median<<<mg, NT, 0, st>>>(a);
+    } else {
+      launch_median(h, a, st, h->S);
+    }
+    h->launches += 1;
+  }
+  return push_outputs(h, a, h->xo, st);
 }
 
 int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_device, void* cuda_stream) {

@@ -38,7 +38,7 @@ constexpr int KMAX = 32;      // largest supported subspace dimension
 constexpr int NT = 256;       // threads per CTA
 constexpr int NW = NT / 32;   // warps per CTA
 #ifndef PROST_WC
-#define PROST_WC 6
+#define PROST_WC 4
 #endif
 #ifndef PROST_MINB
 #define PROST_MINB 2
@@ -96,6 +96,14 @@ struct Args {
   void* res_out;       // [S][np] or null
   uint8_t* raw_out;    // [S][Pp] or null
   uint8_t* mask_out;   // [S][Pp] or null
+  // Pixel-sharded (exchange) mode: a phase kernel's last CTA leaves the
+  // stream's reduced partials in xred[s] (and whether the phase ran for the
+  // stream in xgo[s]) instead of running the scalar logic; the caller sums
+  // xred over ranks and k_xlogic finishes the phase.  Null otherwise.
+  double* xred;        // [S][nvmax]
+  int* xgo;            // [S]
+  const uint8_t* halo_top;  // [S][width] label row above the local rows, or null
+  const uint8_t* halo_bot;  // [S][width] label row below the local rows, or null
   int s0;              // first stream of this launch
   int k, C, P, Pp, width, height;
   long long np;        // padded coordinates per stream = C * Pp
@@ -276,9 +284,15 @@ __device__ __forceinline__ bool cta_finish(const Args& a, int s, double* sm, int
     double acc = 0.0;
     for (int c = 0; c < a.chunks; ++c) acc += __ldcg(base + (size_t)c * a.nvmax + v);
     red[v] = acc;
+    if (a.xred) a.xred[(size_t)s * a.nvmax + v] = acc;  // exchange mode: k_xlogic finishes
   }
   __syncthreads();
-  return true;
+  return a.xred == nullptr;
+}
+
+// Exchange mode: record whether this phase runs for stream s (block 0 only).
+__device__ __forceinline__ void mark_go(const Args& a, int s, int go) {
+  if (a.xgo && blockIdx.x == 0 && threadIdx.x == 0) a.xgo[s] = go;
 }
 
 // ---------------------------------------------------------------------------

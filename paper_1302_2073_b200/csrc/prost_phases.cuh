@@ -61,6 +61,75 @@ __device__ __forceinline__ double running_std(const Ctl* c) {
   return fmax(sqrt(fmax(var, 0.0)), STD_FLOOR);
 }
 
+// Scalar tails of the phases with a reduction (shared by the phase kernels and
+// k_xlogic, which runs them after the cross-rank sum in exchange mode).
+
+// red: [0] sum x, [1] sum x^2, [2] non-finite count (thread 0)
+__device__ __forceinline__ void tail_stats(Ctl* c, const Args& a, int s, const double* red) {
+  if (red[2] > 0.0) {
+    c->status = ST_NONFINITE;
+    c->t = step_size(a, c->frame_index);
+    write_info(c, a, s);
+  } else {
+    c->psum += red[0];
+    c->psumsq += red[1];
+    c->pcount += a.n_real;
+    c->pseen += 1;
+    c->std_cur = running_std(c);
+    c->update_stats = 1;
+    c->status = ST_OK;
+  }
+}
+
+// red: [0..K) U^T x, [K] non-finite count (warp 0)
+template <int K>
+__device__ __forceinline__ void tail_cold(Ctl* c, const Args& a, int s, int lane, const double* red) {
+  if (red[K] > 0.0) {
+    if (lane == 0) {
+      c->status = ST_NONFINITE;
+      c->t = step_size(a, c->frame_index);
+      write_info(c, a, s);
+    }
+  } else if (lane < a.k) {
+    c->y[lane] = red[lane];
+  }
+}
+
+// red: packed upper triangle of U^T U (thread 0): Cholesky R, R^-1, reset the
+// QR counter (manifold.py:192-196)
+__device__ __forceinline__ void tail_gram(Ctl* c, const Args& a, int s, const double* red) {
+  __shared__ double Rm[KMAX * KMAX];
+  const int k = a.k;
+  auto Gat = [&](int i, int j) {
+    if (i > j) { const int t = i; i = j; j = t; }
+    return red[i * k - i * (i - 1) / 2 + (j - i)];
+  };
+  for (int i = 0; i < KMAX * KMAX; ++i) Rm[i] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    double dsum = Gat(j, j);
+    for (int l = 0; l < j; ++l) dsum -= Rm[l * KMAX + j] * Rm[l * KMAX + j];
+    const double rjj = sqrt(fmax(dsum, 1e-300));
+    Rm[j * KMAX + j] = rjj;
+    for (int i = j + 1; i < k; ++i) {
+      double o = Gat(j, i);
+      for (int l = 0; l < j; ++l) o -= Rm[l * KMAX + j] * Rm[l * KMAX + i];
+      Rm[j * KMAX + i] = o / rjj;
+    }
+  }
+  // R^{-1}, upper triangular, column by column
+  double* Ri = a.rinv + (size_t)s * KMAX * KMAX;
+  for (int i = 0; i < KMAX * KMAX; ++i) Ri[i] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    Ri[j * KMAX + j] = 1.0 / Rm[j * KMAX + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double o = 0.0;
+      for (int l = i + 1; l <= j; ++l) o += Rm[i * KMAX + l] * Ri[l * KMAX + j];
+      Ri[i * KMAX + j] = -o / Rm[i * KMAX + i];
+    }
+  }
+  c->since_qr = 0;
+}
+
 // ---------------------------------------------------------------------------
 // k_stats: frame start.  Pipeline frames inside the statistics window fold the
 // raw frame's sums into the running statistics (pipeline.py:120-132) and
@@ -72,6 +141,7 @@ __global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   const bool upd = a.pipeline && !c->frozen && c->frame_index < a.i_init;
+  mark_go(a, s, upd);
   if (!upd) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       double sd = 1.0;
@@ -113,21 +183,7 @@ __global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
   cta_stage(s2, sm, 1, 3);
   cta_stage(nf, sm, 2, 3);
   if (!cta_finish(a, s, sm, 3, red)) return;
-  if (threadIdx.x == 0) {
-    if (red[2] > 0.0) {
-      c->status = ST_NONFINITE;
-      c->t = step_size(a, c->frame_index);
-      write_info(c, a, s);
-    } else {
-      c->psum += red[0];
-      c->psumsq += red[1];
-      c->pcount += a.n_real;
-      c->pseen += 1;
-      c->std_cur = running_std(c);
-      c->update_stats = 1;
-      c->status = ST_OK;
-    }
-  }
+  if (threadIdx.x == 0) tail_stats(c, a, s, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -146,6 +202,7 @@ __global__ void __launch_bounds__(NT) k_cold(const __grid_constant__ Args a) {
     sseen = (double)c->pseen;
   }
   __syncthreads();
+  mark_go(a, s, go);
   if (!go) return;
   __shared__ double sm[NW * (K + 1)];
   __shared__ double red[K + 1];
@@ -179,18 +236,7 @@ __global__ void __launch_bounds__(NT) k_cold(const __grid_constant__ Args a) {
   for (int j = 0; j < K; ++j) cta_stage((double)acc[j], sm, j, K + 1);
   cta_stage(bad ? 1.0 : 0.0, sm, K, K + 1);
   if (!cta_finish(a, s, sm, K + 1, red)) return;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    if (red[K] > 0.0) {
-      if (lane == 0) {
-        c->status = ST_NONFINITE;
-        c->t = step_size(a, c->frame_index);
-        write_info(c, a, s);
-      }
-    } else if (lane < a.k) {
-      c->y[lane] = red[lane];
-    }
-  }
+  if (threadIdx.x < 32) tail_cold<K>(c, a, s, threadIdx.x, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -210,6 +256,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_pass0(const __grid_constant_
   }
   if (threadIdx.x < K) sy[threadIdx.x] = threadIdx.x < a.k ? c->y[threadIdx.x] : 0.0;
   __syncthreads();
+  mark_go(a, s, go);
   if (!go) return;
   constexpr int NV = K + 3;
   __shared__ double sm[NW * NV];
@@ -289,6 +336,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_iter(const __grid_constant__
   }
   if (threadIdx.x < K) sd[threadIdx.x] = threadIdx.x < a.k ? c->d[threadIdx.x] : 0.0;
   __syncthreads();
+  mark_go(a, s, go);
   if (!go) return;
   constexpr int NV = WC + WG * (K + 1);
   __shared__ double sm[NW * NV];
@@ -399,6 +447,7 @@ __global__ void __launch_bounds__(NT) k_lsfb(const __grid_constant__ Args a) {
     m0 = c->ls_next;
   }
   __syncthreads();
+  mark_go(a, s, go);
   if (!go) return;
   __shared__ double sm[NW * LSW];
   __shared__ double red[LSW];
@@ -462,6 +511,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_gradfb(const __grid_constant
     salpha = c->acc_alpha;
   }
   __syncthreads();
+  mark_go(a, s, go);
   if (!go) return;
   constexpr int NV = K + 1;
   __shared__ double sm[NW * NV];
@@ -683,6 +733,7 @@ __global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
   __shared__ int go;
   if (threadIdx.x == 0) go = c->status == ST_OK && c->qr_now;
   __syncthreads();
+  mark_go(a, s, go);
   if (!go) return;
   constexpr int NP = K * (K + 1) / 2;
   __shared__ double sm[NW * NP];
@@ -710,37 +761,7 @@ __global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
     }
   }
   if (!cta_finish(a, s, sm, np_, red)) return;
-  if (threadIdx.x != 0) return;
-  // G (packed upper triangle) is in red; R lives in shared memory.
-  __shared__ double Rm[KMAX * KMAX];
-  auto Gat = [&](int i, int j) {
-    if (i > j) { const int t = i; i = j; j = t; }
-    return red[i * k - i * (i - 1) / 2 + (j - i)];
-  };
-  for (int i = 0; i < KMAX * KMAX; ++i) Rm[i] = 0.0;
-  for (int j = 0; j < k; ++j) {
-    double dsum = Gat(j, j);
-    for (int l = 0; l < j; ++l) dsum -= Rm[l * KMAX + j] * Rm[l * KMAX + j];
-    const double rjj = sqrt(fmax(dsum, 1e-300));
-    Rm[j * KMAX + j] = rjj;
-    for (int i = j + 1; i < k; ++i) {
-      double o = Gat(j, i);
-      for (int l = 0; l < j; ++l) o -= Rm[l * KMAX + j] * Rm[l * KMAX + i];
-      Rm[j * KMAX + i] = o / rjj;
-    }
-  }
-  // R^{-1}, upper triangular, column by column
-  double* Ri = a.rinv + (size_t)s * KMAX * KMAX;
-  for (int i = 0; i < KMAX * KMAX; ++i) Ri[i] = 0.0;
-  for (int j = 0; j < k; ++j) {
-    Ri[j * KMAX + j] = 1.0 / Rm[j * KMAX + j];
-    for (int i = j - 1; i >= 0; --i) {
-      double o = 0.0;
-      for (int l = i + 1; l <= j; ++l) o += Rm[i * KMAX + l] * Ri[l * KMAX + j];
-      Ri[i * KMAX + j] = -o / Rm[i * KMAX + i];
-    }
-  }
-  c->since_qr = 0;
+  if (threadIdx.x == 0) tail_gram(c, a, s, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -757,11 +778,14 @@ __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
     int votes = 0;
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy) {
-      const int ry = min(max(yy + dy, 0), H - 1);
+      const int ry = yy + dy;
+      const uint8_t* row = ry < 0 ? (a.halo_top ? a.halo_top + (size_t)s * W : L)
+                                  : (ry >= H ? (a.halo_bot ? a.halo_bot + (size_t)s * W : L + (size_t)(H - 1) * W)
+                                             : L + (size_t)ry * W);
 #pragma unroll
       for (int dx = -1; dx <= 1; ++dx) {
         const int rx = min(max(xx + dx, 0), W - 1);
-        votes += L[ry * W + rx];
+        votes += row[rx];
       }
     }
     M[p] = votes >= 5 ? 1 : 0;
@@ -780,13 +804,16 @@ __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) 
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
   uint32_t* M = reinterpret_cast<uint32_t*>(a.mask_out + (size_t)s * a.Pp);
   const int nw = wq * H;
+  // rows beyond the local block: a neighbour's halo row (pixel sharding), else
+  // the edge row itself (edge replication)
+  const uint8_t* above = a.halo_top ? a.halo_top + (size_t)s * W : L;
+  const uint8_t* below = a.halo_bot ? a.halo_bot + (size_t)s * W : L + (size_t)(H - 1) * W;
   for (int q = blockIdx.x * NT + threadIdx.x; q < nw; q += gridDim.x * NT) {
     const int yy = q / wq, xq = q - yy * wq, x0 = xq << 2;
-    const int ya = yy > 0 ? yy - 1 : 0, yb = yy < H - 1 ? yy + 1 : H - 1;
     const int xl = x0 > 0 ? x0 - 1 : 0, xr = x0 + 4 < W ? x0 + 4 : W - 1;
-    const uint8_t* ra = L + (size_t)ya * W;
+    const uint8_t* ra = yy > 0 ? L + (size_t)(yy - 1) * W : above;
     const uint8_t* rm = L + (size_t)yy * W;
-    const uint8_t* rb = L + (size_t)yb * W;
+    const uint8_t* rb = yy < H - 1 ? L + (size_t)(yy + 1) * W : below;
     const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(ra + x0)) +
                        __ldg(reinterpret_cast<const uint32_t*>(rm + x0)) +
                        __ldg(reinterpret_cast<const uint32_t*>(rb + x0));
@@ -794,6 +821,33 @@ __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) 
     const uint32_t r = (uint32_t)__ldg(ra + xr) + __ldg(rm + xr) + __ldg(rb + xr);
     const uint32_t win = v + ((v << 8) | l) + ((v >> 8) | (r << 24));
     M[q] = __vcmpgeu4(win, 0x05050505u) & 0x01010101u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_xlogic: exchange mode — the scalar tail of phase `step` for every stream
+// the phase ran for, from the cross-rank sums in xred (one warp per stream).
+
+enum XStep { XS_STATS = 0, XS_COLD, XS_PASS0, XS_ITER, XS_LSFB, XS_GRADFB, XS_GEO, XS_GRAM, XS_GEOQR };
+
+template <int K>
+__global__ void __launch_bounds__(32) k_xlogic(const __grid_constant__ Args a, int step) {
+  const int s = a.s0 + blockIdx.x;
+  if (!a.xgo[s]) return;
+  Ctl* c = a.ctl + s;
+  __shared__ double red[KMAX * (KMAX + 1) / 2 + 8];
+  const int lane = threadIdx.x;
+  for (int v = lane; v < a.nvmax; v += 32) red[v] = a.xred[(size_t)s * a.nvmax + v];
+  __syncwarp();
+  switch (step) {
+    case XS_STATS: if (lane == 0) tail_stats(c, a, s, red); break;
+    case XS_COLD: tail_cold<K>(c, a, s, lane, red); break;
+    case XS_PASS0: after_pass0<K>(c, a, s, lane, red); break;
+    case XS_ITER: after_iter<K>(c, a, s, lane, red, c->gwin_lo); break;
+    case XS_LSFB: after_lsfb(c, a, s, lane, red, c->ls_next); break;
+    case XS_GRADFB: after_gradfb<K>(c, a, s, lane, red); break;
+    case XS_GRAM: if (lane == 0) tail_gram(c, a, s, red); break;
+    default: break;
   }
 }
 

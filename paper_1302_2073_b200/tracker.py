@@ -258,6 +258,14 @@ class NativeTracker:
         """Enqueue one frame per stream.  Outputs are numpy arrays or torch
         tensors (host or device) to fill.  With fit=True the call waits and
         returns the per-stream `prost_fit_info` array."""
+        fp, fdt, fdev, out = self._frame_and_outputs(frames, background, residual, mask,
+                                                     raw_mask, fit)
+        rc = self._lib.prost_push(self._h, fp, fdt, fdev, ctypes.byref(out),
+                                  ctypes.c_void_p(cuda_stream))
+        self._check(rc, "push")
+        return self._fit if fit else None
+
+    def _frame_and_outputs(self, frames, background, residual, mask, raw_mask, fit):
         fp, fdt, fdev, fcount = _buffer(frames)
         if fcount != self.n_streams * self.m:
             raise DimensionError(
@@ -289,10 +297,46 @@ class NativeTracker:
         out.on_device = dev_flags.pop() if dev_flags else 0
         if fit:
             out.fit = ctypes.cast(self._fit, ctypes.POINTER(nat.FitInfo))
-        rc = self._lib.prost_push(self._h, fp, fdt, fdev, ctypes.byref(out),
-                                  ctypes.c_void_p(cuda_stream))
-        self._check(rc, "push")
-        return self._fit if fit else None
+        return fp, fdt, fdev, out
+
+    # -- exchange (pixel-sharded) mode, include/prost_b200.h --------------
+    def set_exchange(self, n_real_global: int) -> None:
+        self._check(self._lib.prost_set_exchange(self._h, int(n_real_global)), "set_exchange")
+
+    def exchange_buffer(self):
+        """(device pointer, element count) of the float64 exchange buffer."""
+        ptr, cnt = ctypes.c_void_p(), ctypes.c_int64()
+        self._check(self._lib.prost_xbuffer(self._h, ctypes.byref(ptr), ctypes.byref(cnt)),
+                    "xbuffer")
+        return ptr.value, cnt.value
+
+    def xbegin(self, frames, background=None, residual=None, mask=None, raw_mask=None,
+               fit: bool = False, cuda_stream: int = 0) -> None:
+        fp, fdt, fdev, out = self._frame_and_outputs(frames, background, residual, mask,
+                                                     raw_mask, fit)
+        self._xout = out  # the handle keeps pointers into it until xfinish
+        self._xfit = fit
+        self._check(self._lib.prost_xbegin(self._h, fp, fdt, fdev, ctypes.byref(out),
+                                           ctypes.c_void_p(cuda_stream)), "xbegin")
+
+    def xnext(self, cuda_stream: int = 0) -> bool:
+        x = ctypes.c_int32()
+        self._check(self._lib.prost_xnext(self._h, ctypes.byref(x), ctypes.c_void_p(cuda_stream)),
+                    "xnext")
+        return bool(x.value)
+
+    def xapply(self, cuda_stream: int = 0) -> None:
+        self._check(self._lib.prost_xapply(self._h, ctypes.c_void_p(cuda_stream)), "xapply")
+
+    def xedges(self, top, bottom, cuda_stream: int = 0) -> None:
+        self._check(self._lib.prost_xedges(self._h, ctypes.c_void_p(top), ctypes.c_void_p(bottom),
+                                           ctypes.c_void_p(cuda_stream)), "xedges")
+
+    def xfinish(self, halo_top=None, halo_bottom=None, cuda_stream: int = 0):
+        self._check(self._lib.prost_xfinish(self._h, ctypes.c_void_p(halo_top),
+                                            ctypes.c_void_p(halo_bottom),
+                                            ctypes.c_void_p(cuda_stream)), "xfinish")
+        return self._fit if self._xfit else None
 
     def background(self, out, cuda_stream: int = 0) -> None:
         p, dt, dev, cnt = _buffer(out, writable=True)
