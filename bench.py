@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--wave", type=int, default=0)
+    ap.add_argument("--pixel-shard", action="store_true",
+                    help="shard one stream's pixel rows over the ranks (default for C4 with N > 1)")
     ap.add_argument("--preroll", type=int, default=None,
                     help="untimed frames before warm-up (default: i_init, i.e. past the statistics window)")
     return ap.parse_args()
@@ -287,7 +289,13 @@ def main():
     P = W * H
     n = P * ch
     k = cfg.subspace_dim
-    stream_ids = shard_streams(rank, S)
+    # C3-style configs shard independent streams over ranks (weak scaling);
+    # one very large stream (C4) shards its pixel rows (strong scaling, NCCL
+    # all-reduce of the phase partials)
+    pixel = args.pixel_shard or (ws > 1 and c.get("shard") == "pixel")
+    if pixel:
+        S = 1
+    stream_ids = [0] if pixel else shard_streams(rank, S)
 
     preroll = cfg.i_init if args.preroll is None else args.preroll
     e2e_frames = 0 if args.no_e2e else 2 + args.steps
@@ -305,30 +313,59 @@ def main():
         # search); the scene model runs on the device
         from paper_1302_2073_b200.synth import DeviceScenes, config_spec
 
-        scenes = DeviceScenes([config_spec(args.config, sid) for sid in stream_ids], f"cuda:{dev}",
-                              seed=1000 + rank)
-        frames_dev = scenes.next_frames(need)
-        del scenes
+        specs = [config_spec(args.config, sid) for sid in stream_ids]
         host = None
-        data_note = (f"synthetic (seeded SURVEY.md §8(d) scene model run on the device: {need} "
-                     "consecutive frames per stream staged in HBM, a new frame every step)")
+        if any(sp.jitter for sp in specs):
+            # camera jitter (C2) is generated on the host (numpy), then staged
+            frames_dev = torch.from_numpy(gen_frames(args.config, stream_ids, need)).to(f"cuda:{dev}")
+            data_note = (f"synthetic (seeded SURVEY.md §8(d) generator on the host: {need} "
+                         "consecutive frames per stream staged in HBM, a new frame every step)")
+        else:
+            scenes = DeviceScenes(specs, f"cuda:{dev}", seed=1000 + rank)
+            frames_dev = scenes.next_frames(need)
+            del scenes
+            data_note = (f"synthetic (seeded SURVEY.md §8(d) scene model run on the device: {need} "
+                         "consecutive frames per stream staged in HBM, a new frame every step)")
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     F = frames_dev.shape[0]
-    bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev)
-    if args.wave:
-        bt.native.set_wave(args.wave)
     from paper_1302_2073_b200 import _native as nat
 
-    mode = bt.native.query(nat.Q_RESIDENT)
-    if mode:
-        kernel_path = (f"{'tmem' if mode == 2 else 'register'}-resident: "
-                       f"{bt.native.query(nat.Q_TEAMS)} teams x "
-                       f"{bt.native.query(nat.Q_TEAM)} CTAs, one cooperative launch per step")
+    if pixel:
+        from paper_1302_2073_b200.shard import ShardedTracker
+
+        st = ShardedTracker(cfg, precision=args.precision, device=dev)
+        native = st.native
+        W_, r0, r1 = W, st.row0, st.row1
+        # this rank's row block of every staged frame
+        frames_dev = torch.cat([frames_dev[:, 0, c_ * P + r0 * W_: c_ * P + r1 * W_]
+                                for c_ in range(ch)], dim=1).contiguous()[:, None, :]
+        P_loc, n_loc = (r1 - r0) * W, (r1 - r0) * W * ch
+
+        def do_push(frame, background, mask):
+            st.push(frame[0], background=background[0], mask=mask[0])
     else:
-        kernel_path = f"streamed: {bt.native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel"
-    mask = torch.empty((S, P), dtype=torch.uint8, device=f"cuda:{dev}")
-    bg = torch.empty((S, n), dtype=torch.float32 if args.precision == "fp32" else torch.float64,
+        bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev)
+        if args.wave:
+            bt.native.set_wave(args.wave)
+        native = bt.native
+        P_loc, n_loc = P, n
+
+        def do_push(frame, background, mask):
+            bt.push(frame, background=background, mask=mask)
+
+    mode = native.query(nat.Q_RESIDENT)
+    if pixel:
+        kernel_path = (f"pixel-sharded: rows {r0}-{r1} of {H} on rank {rank}, streamed phase "
+                       f"kernels, NCCL all-reduce of the phase partials")
+    elif mode:
+        kernel_path = (f"{'tmem' if mode == 2 else 'register'}-resident: "
+                       f"{native.query(nat.Q_TEAMS)} teams x "
+                       f"{native.query(nat.Q_TEAM)} CTAs, one cooperative launch per step")
+    else:
+        kernel_path = f"streamed: {native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel"
+    mask = torch.empty((S, P_loc), dtype=torch.uint8, device=f"cuda:{dev}")
+    bg = torch.empty((S, n_loc), dtype=torch.float32 if args.precision == "fp32" else torch.float64,
                      device=f"cuda:{dev}")
 
     def barrier():
@@ -344,48 +381,49 @@ def main():
     torch.cuda.synchronize()
     t_pre = time.perf_counter()
     for _ in range(preroll):
-        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        do_push(frames_dev[step % F], bg, mask)
         step += 1
     torch.cuda.synchronize()
     t_pre = time.perf_counter() - t_pre
     for _ in range(args.warmup):
-        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        do_push(frames_dev[step % F], bg, mask)
         step += 1
     torch.cuda.synchronize()
-    bt.synchronize()
+    native.synchronize()
 
     clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)).split(",")[0])
                     if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else dev)
     clocks.start()
     time.sleep(0.3)
-    launches0 = bt.native.launches
+    launches0 = native.launches
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        do_push(frames_dev[step % F], bg, mask)
         step += 1
     e1.record()
     torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1)
-    launches = bt.native.launches - launches0
+    launches = native.launches - launches0
     clk = clocks.stop()
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps
-    value = ws * S * args.steps / (ms / 1000.0)
+    units = S if pixel else ws * S  # stream-frames of the whole job
+    value = units * args.steps / (ms / 1000.0)
 
     # per-phase breakdown (separate, untimed pass with events around launches)
-    bt.native.profile(True)
+    native.profile(True)
     for _ in range(3):
-        bt.push(frames_dev[step % F], background=bg, mask=mask)
+        do_push(frames_dev[step % F], bg, mask)
         step += 1
     torch.cuda.synchronize()
-    phases = bt.native.profile_read()
-    resident_counters = bt.native.resident_counters() if bt.native.query(nat.Q_RESIDENT) else None
-    bt.native.profile(False)
+    phases = native.profile_read()
+    resident_counters = native.resident_counters() if native.query(nat.Q_RESIDENT) else None
+    native.profile(False)
 
     # end to end through the public API: pinned host frames in, host mask + bg out
     e2e = None
@@ -400,26 +438,26 @@ def main():
                                       pin_memory=True)
             host_pinned.copy_(frames_dev[e2e0:e2e0 + HF])
 
-        mask_h = torch.empty((S, P), dtype=torch.uint8).pin_memory()
-        bg_h = torch.empty((S, n), dtype=bg.dtype).pin_memory()
+        mask_h = torch.empty((S, P_loc), dtype=torch.uint8).pin_memory()
+        bg_h = torch.empty((S, n_loc), dtype=bg.dtype).pin_memory()
         for _ in range(2):
-            bt.push(host_pinned[(step - e2e0) % HF], background=bg_h, mask=mask_h)
+            do_push(host_pinned[(step - e2e0) % HF], bg_h, mask_h)
             step += 1
         torch.cuda.synchronize()
         barrier()
         e0.record()
         for _ in range(args.steps):
-            bt.push(host_pinned[(step - e2e0) % HF], background=bg_h, mask=mask_h)
+            do_push(host_pinned[(step - e2e0) % HF], bg_h, mask_h)
             step += 1
         e1.record()
         torch.cuda.synchronize()
         barrier()
         ms_e2e = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": ws * S * args.steps / (ms_e2e / 1000.0), "unit": "stream-frames/s",
-               "h2d_bytes_per_step": S * n * host_pinned.element_size(),
-               "d2h_bytes_per_step": S * P + S * n * bg_h.element_size(),
+        e2e = {"value": units * args.steps / (ms_e2e / 1000.0), "unit": "stream-frames/s",
+               "h2d_bytes_per_step": S * n_loc * host_pinned.element_size(),
+               "d2h_bytes_per_step": S * P_loc + S * n_loc * bg_h.element_size(),
                "ms_per_step": ms_e2e / args.steps}
-    bt.synchronize()
+    native.synchronize()
 
     # roofline of the frame update (per GPU)
     peaks_path = ROOT / "MEASURED_PEAKS.json"
@@ -428,9 +466,9 @@ def main():
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     else:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    ba = b_alg(n, k, P)
+    ba = b_alg(n_loc, k, P_loc)  # per GPU: its own streams, or its row block
     achieved = S * ba / (ms_step / 1000.0) / 1e9
-    bu = 8 * n * k
+    bu = 8 * n_loc * k
     traffic = None
     tpath = ROOT / "profiles" / "traffic.json"
     if tpath.exists():
@@ -462,14 +500,14 @@ def main():
         line = {
             "metric": "frames/s", "value": value, "unit": "stream-frames/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if pixel else "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "f64",
             "data": data_note,
             "config": {"workload": f"{args.config}: {S} streams/GPU x {W}x{H}x{ch}, k={k}, "
                                    f"p={cfg.p}, mu={cfg.mu}, cg_max_iters={cfg.cg_max_iters}",
                        "streams_per_gpu": S, "n": n, "k": k, "precision": args.precision,
                        "l2": "inputs larger than L2 (U alone is %.2f GB per GPU)" % (S * 4 * n * k / 1e9),
-                       "parallelism": f"stream-sharded x{ws}",
+                       "parallelism": f"pixel-row-sharded x{ws}" if pixel else f"stream-sharded x{ws}",
                        "kernel_path": kernel_path},
             "mpix_per_s": value * P / 1e6,
             "gpu_launches": launches,

@@ -172,7 +172,7 @@ CONFIGS = {
                             target_width=3840, target_height=2160, grayscale=True),
                scene=dict(width=3840, height=2160, channels=1, rank=10, noise=0.02,
                           area=(0.03, 0.08), max_speed=8),
-               frames=500, streams=1),
+               frames=500, streams=1, shard="pixel"),
 }
 
 
