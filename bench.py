@@ -449,6 +449,7 @@ def main():
         for _ in range(args.steps):
             do_push(host_pinned[(step - e2e0) % HF], bg_h, mask_h)
             step += 1
+        native.join(torch.cuda.current_stream().cuda_stream)  # the last step's copies too
         e1.record()
         torch.cuda.synchronize()
         barrier()

@@ -136,6 +136,10 @@ int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_devic
 /* Wait for all work enqueued by this handle; returns the first per-stream
  * status of the last push (PROST_ERR_NONFINITE if a frame was rejected). */
 int prost_synchronize(prost_handle* h);
+/* Make `cuda_stream` wait for pushes still in flight on the handle's own
+ * streams (a push with host frames and host outputs and no fit info runs
+ * pipelined: upload, kernels and download of consecutive frames overlap). */
+int prost_join(prost_handle* h, void* cuda_stream);
 
 /* Copy the last error message into buf (NUL-terminated); returns its length. */
 int prost_last_error(prost_handle* h, char* buf, int32_t len);

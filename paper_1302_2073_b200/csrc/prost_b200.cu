@@ -97,6 +97,17 @@ struct prost_handle {
   Args xa;
   prost_outputs xo{};
   bool xactive = false;
+  // pipelined host I/O (prost_push with host frames and host outputs): upload
+  // on s_in, kernels on s_comp, download on s_out, double-buffered, so the
+  // copies of one frame overlap the kernels of the next
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_user = nullptr, ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  void* io_x[2] = {};
+  void* io_bg[2] = {};
+  void* io_res[2] = {};
+  uint8_t* io_mask[2] = {};
+  int io_slot = 0, io_last = 0;
+  bool io_pending = false;
   // optional per-phase timing (prost_profile)
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -654,6 +665,113 @@ int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStr
   return PROST_OK;
 }
 
+// The kernels of one frame for every stream on stream `st`.
+int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
+  if (h->resident || h->tmem) {
+    // one cooperative launch for the whole frame of every stream, then the median
+    const char* stg = getenv("PROST_STAGGER_NS");
+    const char* npf = getenv("PROST_NO_PREFETCH");  // "0" enables the (slower, measured) L2 prefetch
+    RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
+             h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, (npf && npf[0] == '0') ? 1 : 0};
+    CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * sizeof(unsigned), st));
+    long long n = 0;
+    {
+      PhaseTimer pt_(h, st, PROST_PH_FRAME);
+      if (h->tmem)
+        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rsmem, st));
+      else
+        CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
+      ++n;
+    }
+    if (h->tmem && h->qr_due) h->ops.qr(h, a, st, h->S);  // per stream: exits unless due
+    if (a.mask_out) {
+      PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
+      launch_median(h, a, st, h->S);
+      ++n;
+    }
+    h->launches += n;
+  } else {
+    const int wave = std::max(1, std::min(h->wave, h->S));
+    for (int s0 = 0; s0 < h->S; s0 += wave) {
+      a.s0 = s0;
+      h->ops.frame(h, a, st, std::min(wave, h->S - s0));
+    }
+  }
+  CK(cudaGetLastError());
+  return PROST_OK;
+}
+
+// Wait for pipelined host-I/O pushes still in flight (before any direct state access).
+int io_drain(prost_handle* h) {
+  if (!h->io_pending) return PROST_OK;
+  CK(cudaStreamSynchronize(h->s_in));
+  CK(cudaStreamSynchronize(h->s_comp));
+  CK(cudaStreamSynchronize(h->s_out));
+  h->io_pending = false;
+  return PROST_OK;
+}
+
+// prost_push with host frames and host outputs: H2D of this frame overlaps the
+// kernels of the previous one, whose D2H overlaps both.  Ordered after the
+// caller's stream `st` at entry; prost_join / prost_synchronize wait for it.
+int push_pipelined(prost_handle* h, const void* frames, int32_t dtype, const prost_outputs* out,
+                   cudaStream_t st) {
+  CK(cudaSetDevice(h->device));
+  if (!h->s_in) {
+    CK(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->s_comp, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_user, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_comp[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
+      cudaError_t e = cudaSuccess;
+      const size_t fbytes = (size_t)h->S * h->np * h->esz;
+      if (i == 0) {  // lazily allocated single buffers are superseded by the slots
+        if (h->bgbuf) cudaFree(h->bgbuf);
+        if (h->resbuf) cudaFree(h->resbuf);
+        if (h->maskbuf) cudaFree(h->maskbuf);
+        h->bgbuf = h->resbuf = nullptr;
+        h->maskbuf = nullptr;
+      }
+      h->io_x[i] = i == 0 ? h->x : dev_alloc(fbytes, &e);
+      if (e == cudaSuccess) h->io_bg[i] = dev_alloc(fbytes, &e);
+      if (e == cudaSuccess) h->io_res[i] = dev_alloc(fbytes, &e);
+      if (e == cudaSuccess) h->io_mask[i] = (uint8_t*)dev_alloc((size_t)h->S * h->Pp, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "I/O buffers: %s", cudaGetErrorString(e));
+    }
+  }
+  const int sl = h->io_slot;
+  // this slot's buffers were last read by the kernels / copies of two frames ago
+  h->x = h->io_x[sl];
+  h->bgbuf = h->io_bg[sl];
+  h->resbuf = h->io_res[sl];
+  h->maskbuf = h->io_mask[sl];
+  CK(cudaEventRecord(h->ev_user, st));
+  CK(cudaStreamWaitEvent(h->s_in, h->ev_user, 0));
+  CK(cudaStreamWaitEvent(h->s_in, h->ev_comp[sl], 0));
+  Args a;
+  prost_outputs o{};
+  int rc = push_setup(h, frames, dtype, 0, out, h->s_in, &a, &o);
+  if (rc) return rc;
+  CK(cudaEventRecord(h->ev_in[sl], h->s_in));
+  CK(cudaStreamWaitEvent(h->s_comp, h->ev_in[sl], 0));
+  CK(cudaStreamWaitEvent(h->s_comp, h->ev_out[sl], 0));
+  if (h->io_pending) CK(cudaStreamWaitEvent(h->s_comp, h->ev_comp[h->io_last], 0));
+  rc = launch_frame(h, a, h->s_comp);
+  if (rc) return rc;
+  CK(cudaEventRecord(h->ev_comp[sl], h->s_comp));
+  CK(cudaStreamWaitEvent(h->s_out, h->ev_comp[sl], 0));
+  rc = push_outputs(h, a, o, h->s_out);
+  if (rc) return rc;
+  CK(cudaEventRecord(h->ev_out[sl], h->s_out));
+  h->io_last = sl;
+  h->io_slot = sl ^ 1;
+  h->io_pending = true;
+  return PROST_OK;
+}
+
 // ===========================================================================
 // C ABI
 
@@ -848,6 +966,25 @@ void prost_destroy(prost_handle* h) {
                   h->rbar, h->rpart, h->rprof, h->xred, h->xgo};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  // pipelined-I/O slot buffers (slot 0's frame buffer is h->x's allocation,
+  // and h->x / bgbuf / resbuf / maskbuf may point at slot buffers)
+  if (h->s_in) {
+    cudaDeviceSynchronize();
+    void* own[] = {h->io_x[1], h->io_bg[0], h->io_bg[1], h->io_res[0], h->io_res[1], h->io_mask[0],
+                   h->io_mask[1]};
+    for (void* b : own)
+      if (b && b != h->x && b != h->bgbuf && b != h->resbuf && b != h->maskbuf) cudaFree(b);
+    if (h->io_x[0] != h->x) cudaFree(h->io_x[0]);
+    cudaStreamDestroy(h->s_in);
+    cudaStreamDestroy(h->s_comp);
+    cudaStreamDestroy(h->s_out);
+    cudaEventDestroy(h->ev_user);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(h->ev_in[i]);
+      cudaEventDestroy(h->ev_comp[i]);
+      cudaEventDestroy(h->ev_out[i]);
+    }
+  }
   if (h->info_h) cudaFreeHost(h->info_h);
   for (auto& pe : h->prof_ev) {
     cudaEventDestroy(pe.second.first);
@@ -859,6 +996,10 @@ void prost_destroy(prost_handle* h) {
 
 int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const double* y,
                          const double* weights, int64_t frame_index, int64_t steps_since_qr) {
+  if (h) {
+    int drc = io_drain(h);
+    if (drc) return drc;
+  }
   int rc = check_stream(h, stream);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
@@ -906,6 +1047,10 @@ int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const
 
 int prost_get_core_state(prost_handle* h, int32_t stream, double* U, double* y, double* weights,
                          int64_t* frame_index, int64_t* steps_since_qr) {
+  if (h) {
+    int drc = io_drain(h);
+    if (drc) return drc;
+  }
   int rc = check_stream(h, stream);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
@@ -939,6 +1084,10 @@ int prost_get_core_state(prost_handle* h, int32_t stream, double* U, double* y, 
 }
 
 int prost_set_preproc(prost_handle* h, int32_t stream, const double* mean, const double* sc) {
+  if (h) {
+    int drc = io_drain(h);
+    if (drc) return drc;
+  }
   int rc = check_stream(h, stream);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
@@ -962,6 +1111,10 @@ int prost_set_preproc(prost_handle* h, int32_t stream, const double* mean, const
 }
 
 int prost_get_preproc(prost_handle* h, int32_t stream, double* mean, double* sc) {
+  if (h) {
+    int drc = io_drain(h);
+    if (drc) return drc;
+  }
   int rc = check_stream(h, stream);
   if (rc) return rc;
   CK(cudaSetDevice(h->device));
@@ -991,38 +1144,18 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Args a;
   prost_outputs o{};
+  const char* nopipe = getenv("PROST_NO_PIPE");
+  if (!on_device && out && !out->on_device && !out->fit && !h->prof && !(nopipe && nopipe[0] == '1'))
+    return push_pipelined(h, frames, dtype, out, st);
+  if (h->io_pending) {  // order after the pipelined pushes before this one
+    CK(cudaStreamWaitEvent(st, h->ev_comp[h->io_last], 0));
+    CK(cudaStreamWaitEvent(st, h->ev_out[h->io_last], 0));
+    h->io_pending = false;
+  }
   int rc0 = push_setup(h, frames, dtype, on_device, out, st, &a, &o);
   if (rc0) return rc0;
-  if (h->resident || h->tmem) {
-    // one cooperative launch for the whole frame of every stream, then the median
-    const char* stg = getenv("PROST_STAGGER_NS");
-    const char* npf = getenv("PROST_NO_PREFETCH");  // "0" enables the (slower, measured) L2 prefetch
-    RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
-             h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, (npf && npf[0] == '0') ? 1 : 0};
-    CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * sizeof(unsigned), st));
-    long long n = 0;
-    {
-      PhaseTimer pt_(h, st, PROST_PH_FRAME);
-      if (h->tmem)
-        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rsmem, st));
-      else
-        CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
-      ++n;
-    }
-    if (h->tmem && h->qr_due) h->ops.qr(h, a, st, h->S);  // per stream: exits unless due
-    if (a.mask_out) {
-      PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
-      launch_median(h, a, st, h->S);
-      ++n;
-    }
-    h->launches += n;
-  } else {
-    const int wave = std::max(1, std::min(h->wave, h->S));
-    for (int s0 = 0; s0 < h->S; s0 += wave) {
-      a.s0 = s0;
-      h->ops.frame(h, a, st, std::min(wave, h->S - s0));
-    }
-  }
+  rc0 = launch_frame(h, a, st);
+  if (rc0) return rc0;
   return push_outputs(h, a, o, st);
 }
 
@@ -1157,6 +1290,10 @@ int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_devic
   if (!h) return PROST_ERR_CONFIG;
   if (!out) return fail(h, PROST_ERR_DIMENSION, "out is NULL");
   if (!h->pipeline) return fail(h, PROST_ERR_CONFIG, "background_frame needs a pipeline handle");
+  {
+    int drc = io_drain(h);
+    if (drc) return drc;
+  }
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int odt = dtype == PROST_F64 ? PROST_F64 : PROST_F32;
@@ -1179,10 +1316,21 @@ int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_devic
   return PROST_OK;
 }
 
+int prost_join(prost_handle* h, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (!h->io_pending) return PROST_OK;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CK(cudaStreamWaitEvent(st, h->ev_comp[h->io_last], 0));
+  CK(cudaStreamWaitEvent(st, h->ev_out[h->io_last], 0));
+  return PROST_OK;
+}
+
 int prost_synchronize(prost_handle* h) {
   if (!h) return PROST_ERR_CONFIG;
   CK(cudaSetDevice(h->device));
   CK(cudaDeviceSynchronize());
+  h->io_pending = false;
   CK(cudaMemcpy(h->info_h, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost));
   for (int s = 0; s < h->S; ++s) {
     if (h->info_h[s].status != PROST_OK) {

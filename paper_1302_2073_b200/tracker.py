@@ -348,6 +348,10 @@ class NativeTracker:
     def synchronize(self) -> None:
         self._check(self._lib.prost_synchronize(self._h), "synchronize")
 
+    def join(self, cuda_stream: int = 0) -> None:
+        """Make `cuda_stream` wait for pipelined host-I/O pushes in flight."""
+        self._check(self._lib.prost_join(self._h, ctypes.c_void_p(cuda_stream)), "join")
+
     def query(self, what: int) -> int:
         v = ctypes.c_int64()
         self._check(self._lib.prost_query(self._h, what, ctypes.byref(v)), "query")
@@ -592,3 +596,8 @@ class BatchTracker:
 
     def synchronize(self) -> None:
         self.native.synchronize()
+
+    def join(self, cuda_stream: int = 0) -> None:
+        """Order `cuda_stream` after every push so far (host-I/O pushes run on
+        the handle's own streams, pipelined)."""
+        self.native.join(cuda_stream)

@@ -348,3 +348,38 @@ def test_resident_kernels_match_streamed(mode, monkeypatch):
     for s in range(S):
         assert sine(U1[s], U2[s]) <= 1e-4
         assert c1[s] == pytest.approx(c2[s], rel=1e-5)
+
+
+@pytest.mark.gpu
+def test_pipelined_host_io_matches_device_io():
+    """Host frames in / host outputs out run pipelined on the handle's own
+    streams (copies of one frame overlap the kernels of the next); the results
+    equal the device-buffer path's, frame after frame and back to back."""
+    import torch
+
+    W, H, S, F = 64, 48, 4, 9
+    cfg = pkg.RunConfig(subspace_dim=8, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=4, seed=0)
+    data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1).astype(np.float32)
+    dev_bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    host_bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    mask_d = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+    bg_d = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
+    frames_h = [torch.from_numpy(data[f]).pin_memory() for f in range(F)]
+    mask_h = [torch.empty((S, W * H), dtype=torch.uint8).pin_memory() for _ in range(F)]
+    bg_h = [torch.empty((S, W * H), dtype=torch.float32).pin_memory() for _ in range(F)]
+    ref_masks, ref_bgs = [], []
+    for f in range(F):
+        dev_bt.push(torch.from_numpy(data[f]).cuda(), background=bg_d, mask=mask_d)
+        ref_masks.append(mask_d.cpu().numpy())
+        ref_bgs.append(bg_d.cpu().numpy())
+    for f in range(F):  # back to back, every frame its own output buffers
+        host_bt.push(frames_h[f], background=bg_h[f], mask=mask_h[f])
+    host_bt.join()
+    torch.cuda.synchronize()
+    for f in range(F):
+        np.testing.assert_array_equal(mask_h[f].numpy(), ref_masks[f])
+        np.testing.assert_array_equal(bg_h[f].numpy(), ref_bgs[f])
+    U_d = dev_bt.native.get_core_state(0)[0]
+    U_h = host_bt.native.get_core_state(0)[0]
+    np.testing.assert_array_equal(U_h, U_d)
