@@ -670,9 +670,9 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
   if (h->resident || h->tmem) {
     // one cooperative launch for the whole frame of every stream, then the median
     const char* stg = getenv("PROST_STAGGER_NS");
-    const char* npf = getenv("PROST_NO_PREFETCH");  // "0" enables the (slower, measured) L2 prefetch
+    const char* pfe = getenv("PROST_PREFETCH");  // k_tmem L2 prefetch point (see prost_tmem.cuh)
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
-             h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, (npf && npf[0] == '0') ? 1 : 0};
+             h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0};
     CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * sizeof(unsigned), st));
     long long n = 0;
     {
