@@ -21,7 +21,9 @@ KEYS = [
 
 
 def launches(path):
+    """{kernel: [duration us per launch]} plus {kernel: [dram bytes per launch]}."""
     agg = collections.OrderedDict()
+    dram = collections.defaultdict(list)
     hdr = None
     for r in csv.reader(open(path)):
         if r and r[0] == "ID":
@@ -30,13 +32,20 @@ def launches(path):
         if not hdr or len(r) != len(hdr):
             continue
         d = dict(zip(hdr, r))
-        if d.get("Metric Name") != "gpu__time_duration.sum":
-            continue
         name = d["Kernel Name"].split("(")[0].replace("void ", "")
-        unit = d.get("Metric Unit", "nsecond")
+        metric = d.get("Metric Name")
+        unit = d.get("Metric Unit", "")
         v = float(d["Metric Value"].replace(",", ""))
-        v = v / 1000.0 if unit.startswith("n") else (v if unit.startswith("u") else v * 1000.0)
-        agg.setdefault(name, []).append(v)
+        if metric == "gpu__time_duration.sum":
+            v = v / 1000.0 if unit.startswith("n") else (v if unit.startswith("u") else v * 1000.0)
+            agg.setdefault(name, []).append(v)
+        elif metric in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            dram[(name, d["ID"])].append(v * scale)
+    per = collections.defaultdict(list)
+    for (name, _), vs in dram.items():
+        per[name].append(sum(vs))
+    launches.dram = per
     return agg
 
 
@@ -69,11 +78,18 @@ def main():
         lines += [a.note, ""]
     if a.launches:
         agg = launches(a.launches)
+        # only this library's kernels: the benchmark's input generation (torch
+        # / cuBLAS) runs before the timed region
+        agg = collections.OrderedDict((k, v) for k, v in agg.items() if k.startswith("prost::"))
         tot = sum(sum(v) for v in agg.values()) or 1.0
         lines += ["## Launch list (ncu `gpu__time_duration.sum`, `--clock-control none`; cold-cache, serialised)", "",
-                  "| kernel | launches | avg us | total us | share |", "|---|---|---|---|---|"]
+                  "| kernel | launches | avg us | total us | share | DRAM MB / launch |",
+                  "|---|---|---|---|---|---|"]
+        dram = getattr(launches, "dram", {})
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-            lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v):.1f} | {sum(v)/tot:.3f} |")
+            d = dram.get(k)
+            dm = f"{sum(d) / len(d) / 1e6:.1f}" if d else "-"
+            lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v):.1f} | {sum(v)/tot:.3f} | {dm} |")
         lines.append("")
     for r in a.rep:
         for kn, d in rep(r):
