@@ -670,7 +670,7 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
   if (h->resident || h->tmem) {
     // one cooperative launch for the whole frame of every stream, then the median
     const char* stg = getenv("PROST_STAGGER_NS");
-    const char* pfe = getenv("PROST_PREFETCH");  // k_tmem L2 prefetch point (see prost_tmem.cuh)
+    const char* pfe = getenv("PROST_PREFETCH");  // 1: k_tmem L2 prefetch of the next stream (measured slower)
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
              h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0};
     CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * sizeof(unsigned), st));
@@ -812,7 +812,11 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const long long groups = (h->Pp / h->ops.VEC + NT - 1) / NT;
-  const long long target = (long long)sms * 8 * 2;
+  // Streamed phase kernels: CTAs per stream.  Many streams: ~16 CTAs per SM
+  // in total (waves keep the HBM queues full); few large streams: one wave of
+  // resident CTAs (the phase kernels are limited to 2 per SM by registers)
+  // with grid-stride loops, so the last CTA sums few partial slots.
+  const long long target = (long long)sms * (h->S >= sms ? 16 : 2);
   h->chunks = (int)std::max<long long>(1, std::min<long long>(groups, (target + h->S - 1) / h->S));
   h->wave = h->S;
   cudaError_t e = cudaSuccess;

@@ -279,14 +279,35 @@ __device__ __forceinline__ bool cta_finish(const Args& a, int s, double* sm, int
   __syncthreads();
   if (!last) return false;
   __threadfence();
+  // Sum the chunk slots in a fixed order with the whole CTA: lane = value
+  // (32 at a time), warp w = chunks w, w + NW, ... (four independent loads in
+  // flight per lane), then the NW warp sums in warp order.
   const double* base = a.part + (size_t)s * a.chunks * a.nvmax;
-  for (int v = threadIdx.x; v < nv; v += NT) {
-    double acc = 0.0;
-    for (int c = 0; c < a.chunks; ++c) acc += __ldcg(base + (size_t)c * a.nvmax + v);
-    red[v] = acc;
-    if (a.xred) a.xred[(size_t)s * a.nvmax + v] = acc;  // exchange mode: k_xlogic finishes
+  __shared__ double wsum[NW][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int v0 = 0; v0 < nv; v0 += 32) {
+    const int v = v0 + lane;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    if (v < nv) {
+      int c = warp;
+      for (; c + 3 * NW < a.chunks; c += 4 * NW) {
+        acc0 += __ldcg(base + (size_t)c * a.nvmax + v);
+        acc1 += __ldcg(base + (size_t)(c + NW) * a.nvmax + v);
+        acc2 += __ldcg(base + (size_t)(c + 2 * NW) * a.nvmax + v);
+        acc3 += __ldcg(base + (size_t)(c + 3 * NW) * a.nvmax + v);
+      }
+      for (; c < a.chunks; c += NW) acc0 += __ldcg(base + (size_t)c * a.nvmax + v);
+    }
+    wsum[warp][lane] = (acc0 + acc1) + (acc2 + acc3);
+    __syncthreads();
+    if (warp == 0 && v < nv) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w) acc += wsum[w][lane];
+      red[v] = acc;
+      if (a.xred) a.xred[(size_t)s * a.nvmax + v] = acc;  // exchange mode: k_xlogic finishes
+    }
+    __syncthreads();
   }
-  __syncthreads();
   return a.xred == nullptr;
 }
 
