@@ -546,6 +546,55 @@ class StreamTracker:
             raise ConfigError("no frames pushed yet")
         return self._native.get_preproc(0)
 
+    # -- PROSTSNAP1 snapshots (jobs.py:241-277, tracker.py:184-285) -----------
+    def snapshot_bytes(self) -> bytes:
+        from .snapshot import pack_snapshot
+
+        if self._native is None:
+            raise ConfigError("no frames pushed yet; nothing to snapshot")
+        return pack_snapshot(self.state, self.params)
+
+    def save(self, path) -> None:
+        with open(path, "wb") as fh:
+            fh.write(self.snapshot_bytes())
+
+    def _adopt(self, U, y, weights, frame_index, pre) -> None:
+        # jobs.py:251-263: the snapshot's dimension fixes the channel count
+        pixels = self.config.target_width * self.config.target_height
+        channels, remainder = divmod(U.shape[0], pixels)
+        if remainder or channels not in (1, 3):
+            raise ConfigError(
+                f"snapshot dimension {U.shape[0]} does not match "
+                f"{self.config.target_width}x{self.config.target_height} frames")
+        w, hgt = self.config.target_width, self.config.target_height
+        self.channels = channels
+        self._native = NativeTracker(self.params, w, hgt, channels, 1, i_init=self.i_init,
+                                     pipeline=True, precision=self.precision, device=self.device)
+        self._native.set_core_state(0, np.ascontiguousarray(U), y, weights, int(frame_index), 0)
+        if pre is None:
+            pre = PreprocSnapshot(mean=np.zeros(U.shape[0]))
+        self._native.set_preproc(0, pre)
+        self._frame_index = int(frame_index)
+
+    @classmethod
+    def restore_bytes(cls, blob: bytes, config: RunConfig, i_init: Optional[int] = None,
+                      **kw) -> "StreamTracker":
+        from .snapshot import unpack_snapshot
+
+        tracker = cls(config, i_init=i_init, **kw)
+        tracker._adopt(*unpack_snapshot(blob, tracker.params))
+        return tracker
+
+    @classmethod
+    def restore(cls, path, config: RunConfig, i_init: Optional[int] = None, **kw) -> "StreamTracker":
+        from .snapshot import unpack_snapshot
+
+        with open(path, "rb") as fh:
+            blob = fh.read()
+        tracker = cls(config, i_init=i_init, **kw)
+        tracker._adopt(*unpack_snapshot(blob, tracker.params, source=str(path)))
+        return tracker
+
 
 # ---------------------------------------------------------------------------
 # many independent streams per launch

@@ -140,6 +140,29 @@ def push_run(name, channels, n_frames=14, i_init=5):
          cfg=np.array([4, 0.5, 1e-4, 2, i_init, 9, channels]))
 
 
+def snapshot_run(n_before=8, n_after=6, i_init=5):
+    """PROSTSNAP1 bytes of a gray StreamTracker after n_before frames, and the
+    reference's continuation after restore_bytes (jobs.py:241-277)."""
+    spec = SceneSpec(width=32, height=24, channels=1, rank=3, n_objects=(2, 2), seed=31, fg_from=2)
+    raw = SceneStream(spec).next_frames(n_before + n_after)
+    cfg = RunConfig(subspace_dim=4, p=0.5, mu=1e-4, cg_max_iters=2, target_width=32,
+                    target_height=24, grayscale=True, i_init=i_init, seed=4)
+    tr = StreamTracker(cfg)
+    for v in raw[:n_before]:
+        tr.push(FrameBuffer(32, 24, 1, v))
+    blob = tr.snapshot_bytes()
+    tr2 = StreamTracker.restore_bytes(blob, cfg)
+    masks, bgs, costs = [], [], []
+    for v in raw[n_before:]:
+        rec = tr2.push(FrameBuffer(32, 24, 1, v))
+        masks.append(rec.mask.labels)
+        costs.append(rec.fit_cost)
+        bgs.append(tr2.background_frame().data)
+    save("snapshot_gray", frames=raw, blob=np.frombuffer(blob, dtype=np.uint8),
+         mask=np.array(masks), background=np.array(bgs), fit_cost=np.array(costs),
+         cfg=np.array([4, 0.5, 1e-4, 2, i_init, 4, n_before]))
+
+
 if __name__ == "__main__":
     print("reference prost", prost.__version__, "numpy", np.__version__)
     cost_vectors()
@@ -148,3 +171,4 @@ if __name__ == "__main__":
     qr_chain()
     push_run("push_gray", 1)
     push_run("push_rgb", 3)
+    snapshot_run()
