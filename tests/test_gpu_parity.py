@@ -383,3 +383,27 @@ def test_pipelined_host_io_matches_device_io():
     U_d = dev_bt.native.get_core_state(0)[0]
     U_h = host_bt.native.get_core_state(0)[0]
     np.testing.assert_array_equal(U_h, U_d)
+
+
+@pytest.mark.gpu
+def test_u8_frame_ingest():
+    """8-bit frames are divided by 255 on load (frameio.py:136, SURVEY §8(f)
+    row 1): the same result as pushing the scaled float32 frames."""
+    import torch
+
+    W, H, S, F = 64, 48, 3, 6
+    cfg = pkg.RunConfig(subspace_dim=8, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=3, seed=0)
+    data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1)
+    q = np.clip(np.rint(data * 255.0), 0, 255).astype(np.uint8)
+    scaled = (q.astype(np.float64) * (1.0 / 255.0)).astype(np.float32)
+    outs = []
+    for frames in (q, scaled):
+        bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
+        for f in range(F):
+            bt.push(torch.from_numpy(frames[f]).cuda(), background=bg, mask=mask)
+        outs.append((mask.cpu().numpy(), bg.cpu().numpy()))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
