@@ -44,7 +44,10 @@ constexpr int NW = NT / 32;   // warps per CTA
 #define PROST_MINB 2
 #endif
 constexpr int WC = PROST_WC;  // Armijo trial costs evaluated per U pass
-constexpr int WG = 2;         // speculative gradients per U pass
+#ifndef PROST_WG
+#define PROST_WG 2
+#endif
+constexpr int WG = PROST_WG;  // speculative gradients per U pass
 constexpr int LSW = 16;       // trial costs per fallback line-search pass
 constexpr int MAXBT = 64;     // cap on CgOptions.max_backtracks
 constexpr int QR_EVERY = 1000;        // manifold.py:40

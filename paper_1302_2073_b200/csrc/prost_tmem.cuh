@@ -36,6 +36,7 @@
 #define PROST_TM_CPS 1
 #endif
 
+
 namespace prost {
 
 // threads per CTA: 4 warps per 128-column TMEM block (one per lane quarter);
