@@ -147,6 +147,11 @@ template <> struct VecIO<float, 2> {
     *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
   }
 };
+template <> struct VecIO<float, 1> {
+  static __device__ __forceinline__ void ld(const float* p, float (&o)[1]) { o[0] = *p; }
+  static __device__ __forceinline__ void ldg(const float* p, float (&o)[1]) { o[0] = __ldg(p); }
+  static __device__ __forceinline__ void st(float* p, const float (&o)[1]) { *p = o[0]; }
+};
 template <> struct VecIO<double, 2> {
   static __device__ __forceinline__ void ld(const double* p, double (&o)[2]) {
     double2 a = *reinterpret_cast<const double2*>(p);

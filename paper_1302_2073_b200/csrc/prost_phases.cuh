@@ -341,9 +341,18 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_iter(const __grid_constant__
   constexpr int NV = WC + WG * (K + 1);
   __shared__ double sm[NW * NV];
   __shared__ double red[NV];
-  T d[K];
+  // large k: the direction stays in shared memory (broadcast reads) so that
+  // u, the two speculative gradients and d do not exceed the register budget
+  constexpr bool DSM = K > 16;
+  __shared__ T sdt[K];
+  T d[DSM ? 1 : K];
+  if (DSM) {
+    if (threadIdx.x < K) sdt[threadIdx.x] = (T)sd[threadIdx.x];
+    __syncthreads();
+  } else {
 #pragma unroll
-  for (int j = 0; j < K; ++j) d[j] = (T)sd[j];
+    for (int j = 0; j < (DSM ? 1 : K); ++j) d[j] = (T)sd[j];
+  }
   T al[WC];
   {
     double v = a.step0;
@@ -395,8 +404,9 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_iter(const __grid_constant__
 #pragma unroll
           for (int e = 0; e < VEC; ++e) u[j][e] = (T)0;
         }
+        const T dj = DSM ? sdt[j] : d[DSM ? 0 : j];
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) ud[e] += u[j][e] * d[j];
+        for (int e = 0; e < VEC; ++e) ud[e] += u[j][e] * dj;
       }
       VecIO<T, VEC>::st(UD + off, ud);
 #pragma unroll
