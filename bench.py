@@ -321,7 +321,8 @@ def main():
             data_note = (f"synthetic (seeded SURVEY.md §8(d) generator on the host: {need} "
                          "consecutive frames per stream staged in HBM, a new frame every step)")
         else:
-            scenes = DeviceScenes(specs, f"cuda:{dev}", seed=1000 + rank)
+            # a pixel-sharded stream is the same stream on every rank
+            scenes = DeviceScenes(specs, f"cuda:{dev}", seed=1000 + (0 if pixel else rank))
             frames_dev = scenes.next_frames(need)
             del scenes
             data_note = (f"synthetic (seeded SURVEY.md §8(d) scene model run on the device: {need} "
