@@ -407,6 +407,7 @@ TmOps pick_tmem(int K, bool half) {
     case 8: return half ? Tm<8, PM_HALF>::ops() : Tm<8, PM_ANY>::ops();
     case 15: return half ? Tm<15, PM_HALF>::ops() : Tm<15, PM_ANY>::ops();
     case 16: return half ? Tm<16, PM_HALF>::ops() : Tm<16, PM_ANY>::ops();
+    case 20: return half ? Tm<20, PM_HALF>::ops() : Tm<20, PM_ANY>::ops();
     default: return TmOps{nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   }
 }
@@ -850,7 +851,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   const char* kenv = getenv("PROST_KERNEL");
   std::string kpath = kenv ? kenv : (want_res && want_res[0] == '1' ? "resident" : "tmem");
   if (no_res && no_res[0] == '1') kpath = "streamed";
-  const bool eligible = !h->fp64 && h->C == 1 && K <= 16;
+  const bool eligible = !h->fp64 && h->C == 1 && K <= 20;
   const TmOps to = pick_tmem(K, params->p == 0.5);
   if (eligible && kpath == "tmem" && to.launch) {
     if (getenv("PROST_DEBUG")) to.describe();

@@ -48,7 +48,7 @@ static_assert(TM_NT == 128 || TM_NT == 256 || TM_NT == 512, "TMEM allocation is 
 template <int K>
 struct TmemGeom {
   // columns per row (power of two >= k: every tcgen05 access is width-aligned)
-  static constexpr int RS = K <= 4 ? 4 : (K <= 8 ? 8 : 16);
+  static constexpr int RS = K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 16 ? 16 : 32));
   static constexpr int QW = 4 * RS;     // columns per row group
   static constexpr int QT = 128 / QW;   // row groups per thread in TMEM
   static constexpr bool WCOL = K < RS;  // weight stored in column RS-1
@@ -72,13 +72,15 @@ __host__ __device__ constexpr size_t tmem_smem(int qpc) {
 
 template <int RS>
 __device__ __forceinline__ void tmem_ld_row(unsigned taddr, float (&v)[RS]) {
-  if constexpr (RS == 16) tmem_ld16(taddr, v);
+  if constexpr (RS == 32) tmem_ld32(taddr, v);
+  else if constexpr (RS == 16) tmem_ld16(taddr, v);
   else if constexpr (RS == 8) tmem_ld8(taddr, v);
   else tmem_ld4(taddr, v);
 }
 template <int RS>
 __device__ __forceinline__ void tmem_st_row(unsigned taddr, const float (&v)[RS]) {
-  if constexpr (RS == 16) tmem_st16(taddr, v);
+  if constexpr (RS == 32) tmem_st32(taddr, v);
+  else if constexpr (RS == 16) tmem_st16(taddr, v);
   else if constexpr (RS == 8) tmem_st8(taddr, v);
   else tmem_st4(taddr, v);
 }

@@ -317,6 +317,33 @@ def test_large_batch_properties():
         assert np.linalg.norm(U.T @ U - np.eye(15)) < 1e-4
 
 
+@pytest.mark.gpu
+def test_tmem_k20_matches_streamed(monkeypatch):
+    """k = 20 (BASELINE C2) runs on the TMEM kernel with 32-column rows and
+    agrees with the streamed kernels."""
+    import torch
+    from paper_1302_2073_b200 import _native as nat
+
+    W, H, S, F = 320, 240, 2, 8
+    cfg = pkg.RunConfig(subspace_dim=20, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=4, seed=0)
+    data = [c0_stream(F, W, H, seed=s) for s in range(S)]
+    out = {}
+    for path, code in (("tmem", 2), ("streamed", 0)):
+        monkeypatch.setenv("PROST_KERNEL", path)
+        bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        assert bt.native.query(nat.Q_RESIDENT) == code
+        mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
+        for f in range(F):
+            fr = torch.from_numpy(np.stack([d[f] for d in data]).astype(np.float32)).cuda()
+            bt.push(fr, background=bg, mask=mask)
+        out[path] = (mask.cpu().numpy(), bg.cpu().numpy())
+    (m1, b1), (m2, b2) = out["tmem"], out["streamed"]
+    assert np.mean(m1 != m2) <= 0.001
+    assert np.linalg.norm(b1 - b2) <= 1e-5 * np.linalg.norm(b2)
+
+
 @pytest.mark.parametrize("mode", ["tmem", "resident"])
 def test_resident_kernels_match_streamed(mode, monkeypatch):
     """The TMEM-resident (default for fp32 single-channel streams) and the
