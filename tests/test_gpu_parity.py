@@ -434,3 +434,32 @@ def test_u8_frame_ingest():
         outs.append((mask.cpu().numpy(), bg.cpu().numpy()))
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("shape", [(30, 17), (41, 9)])
+def test_ragged_shapes_against_oracle(precision, shape):
+    """Widths that are not a multiple of 4 (byte-wise median path) and pixel
+    counts that need padding (P % 4 != 0: padded rows carry weight 0), through
+    the statistics window, against the oracle (fp32 runs the TMEM kernel)."""
+    W, H = shape
+    n_frames, i_init = 14, 5
+    frames = c0_stream(n_frames, W, H, seed=5)
+    cfg = pkg.RunConfig(subspace_dim=4, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=i_init, seed=2)
+    tr = pkg.StreamTracker(cfg, precision=precision)
+    ref = oracle_for(cfg, i_init, W, H)
+    worst = 0.0
+    for v in frames:
+        a = tr.push(pkg.FrameBuffer(W, H, 1, v))
+        b = ref.push(v)
+        worst = max(worst, float(np.mean(a.mask.labels != b.mask)))
+        if precision == "fp64":
+            np.testing.assert_array_equal(a.raw_mask.labels, b.raw_mask)
+            np.testing.assert_array_equal(a.mask.labels, b.mask)
+    rel = np.linalg.norm(tr.background_frame().data - ref.background()) / np.linalg.norm(ref.background())
+    ang = sine(tr.state.basis.data, ref.state.U)
+    if precision == "fp64":
+        assert rel <= 1e-10 and ang <= 1e-9
+    else:
+        assert worst <= 0.01 and rel <= 1e-4 and ang <= 1e-3
