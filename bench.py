@@ -346,7 +346,8 @@ def main():
         def do_push(frame, background, mask):
             st.push(frame[0], background=background[0], mask=mask[0])
     else:
-        bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev)
+        # one stream per GPU: lay the resident kernel out for latency
+        bt = pkg.BatchTracker(cfg, S, precision=args.precision, device=dev, latency=S == 1)
         if args.wave:
             bt.native.set_wave(args.wave)
         native = bt.native

@@ -59,6 +59,10 @@ extern "C" {
 /* handle flags */
 #define PROST_FLAG_PIPELINE 1u  /* StreamTracker semantics: running-stats normalization,
                                    threshold (segment), 3x3 median, per-pixel weights */
+#define PROST_FLAG_LATENCY 4u   /* lay the resident kernel out for the latency of one frame of a
+                                   few streams (more CTAs per stream) instead of the throughput
+                                   of many; per-stream results do not depend on the batch within
+                                   either layout */
 #define PROST_FLAG_FP64 2u      /* double-precision state and per-element arithmetic
                                    (parity instantiation); default is fp32 */
 

@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("PROST_LIB") or
 PROST_OK = 0
 ERR_CONFIG, ERR_DIMENSION, ERR_NONFINITE, ERR_SEQUENCE, ERR_CUDA = 1, 2, 3, 4, 5
 F32, F64, U8 = 0, 1, 2
-FLAG_PIPELINE, FLAG_FP64 = 1, 2
+FLAG_PIPELINE, FLAG_FP64, FLAG_LATENCY = 1, 2, 4
 Q_LAUNCHES, Q_WAVE, Q_BYTES_U, Q_CHUNKS, Q_INSTANCE_K = 0, 1, 2, 3, 4
 Q_RESIDENT, Q_TEAM, Q_TEAMS = 5, 6, 7
 

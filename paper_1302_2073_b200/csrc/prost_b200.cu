@@ -871,7 +871,11 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
       if ((nq + qpc - 1) / qpc != G) continue;
       const size_t sm = to.smem(qpc);
       if (sm > (size_t)227 * 1024) continue;
-      const double cost = (1.5 + (qpc + TM_NT - 1) / TM_NT) / (double)(sms * TM_CPS / G);
+      const int slots = (qpc + TM_NT - 1) / TM_NT;
+      // throughput: teams / round time; latency (PROST_FLAG_LATENCY): the round
+      // time of one stream, slots per thread plus a small per-CTA barrier cost
+      const double cost = (flags & PROST_FLAG_LATENCY) ? slots + 0.05 * G
+                                                       : (1.5 + slots) / (double)(sms * TM_CPS / G);
       if (bestG == 0 || cost < best_cost) {
         bestG = G;
         best_cost = cost;

@@ -172,7 +172,7 @@ class NativeTracker:
 
     def __init__(self, params: ProstParams, width: int, height: int, channels: int,
                  n_streams: int = 1, i_init: int = DEFAULT_I_INIT, pipeline: bool = True,
-                 precision: str = "fp32", device: int = 0):
+                 precision: str = "fp32", device: int = 0, latency: bool = False):
         if precision not in PRECISIONS:
             raise ConfigError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
         self._lib = nat.lib()
@@ -183,7 +183,8 @@ class NativeTracker:
         self.pipeline = pipeline
         self.m = width * height * channels
         self.pixels = width * height
-        flags = PRECISIONS[precision] | (nat.FLAG_PIPELINE if pipeline else 0)
+        flags = (PRECISIONS[precision] | (nat.FLAG_PIPELINE if pipeline else 0)
+                 | (nat.FLAG_LATENCY if latency else 0))
         h = ctypes.c_void_p()
         native = to_native(params, width, height, channels, i_init)
         rc = self._lib.prost_create(ctypes.byref(native), n_streams, flags, device, ctypes.byref(h))
@@ -490,7 +491,8 @@ class StreamTracker:
         w, hgt = self.config.target_width, self.config.target_height
         self.channels = channels
         self._native = NativeTracker(self.params, w, hgt, channels, 1, i_init=self.i_init,
-                                     pipeline=True, precision=self.precision, device=self.device)
+                                     pipeline=True, precision=self.precision, device=self.device,
+                                     latency=True)
         m = w * hgt * channels
         U0 = random_orthonormal(m, self.params.k, self.config.seed).data
         self._native.set_core_state(0, U0, np.zeros(self.params.k), None, 0, 0)
@@ -569,7 +571,8 @@ class StreamTracker:
         w, hgt = self.config.target_width, self.config.target_height
         self.channels = channels
         self._native = NativeTracker(self.params, w, hgt, channels, 1, i_init=self.i_init,
-                                     pipeline=True, precision=self.precision, device=self.device)
+                                     pipeline=True, precision=self.precision, device=self.device,
+                                     latency=True)
         self._native.set_core_state(0, np.ascontiguousarray(U), y, weights, int(frame_index), 0)
         if pre is None:
             pre = PreprocSnapshot(mean=np.zeros(U.shape[0]))
@@ -613,7 +616,7 @@ class BatchTracker:
 
     def __init__(self, config: RunConfig, n_streams: int, i_init: Optional[int] = None, *,
                  seeds: Optional[Sequence[int]] = None, precision: str = "fp32",
-                 device: int = 0, init_bases: bool = True):
+                 device: int = 0, init_bases: bool = True, latency: bool = False):
         self.config = config
         self.i_init = i_init if i_init is not None else (
             config.i_init if config.i_init is not None else DEFAULT_I_INIT)
@@ -622,7 +625,7 @@ class BatchTracker:
         self.n_streams = n_streams
         self.native = NativeTracker(self.params, config.target_width, config.target_height,
                                     self.channels, n_streams, i_init=self.i_init, pipeline=True,
-                                    precision=precision, device=device)
+                                    precision=precision, device=device, latency=latency)
         self.m = self.native.m
         self.pixels = self.native.pixels
         seeds = list(seeds) if seeds is not None else [config.seed] * n_streams
