@@ -67,6 +67,7 @@ struct prost_handle {
   void* x = nullptr;
   void* mean = nullptr;
   uint8_t* lab = nullptr;
+  uint8_t* labc = nullptr;  // 3-channel TMEM path: per-coordinate label flags
   Ctl* ctl = nullptr;
   double* part = nullptr;
   unsigned* cnt = nullptr;
@@ -151,6 +152,7 @@ Args make_args(prost_handle* h, int s0) {
   a.x = h->x;
   a.mean = h->mean;
   a.lab = h->lab;
+  a.labc = h->labc;
   a.ctl = h->ctl;
   a.part = h->part;
   a.cnt = h->cnt;
@@ -684,6 +686,11 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
         CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
       ++n;
     }
+    if (h->tmem && h->C == 3) {  // labels: any channel over the threshold
+      const dim3 cg(std::max(1, std::min((h->Pp / 4 + NT - 1) / NT, 64)), h->S);
+      k_combine3<<<cg, NT, 0, st>>>(a);
+      ++n;
+    }
     if (h->tmem && h->qr_due) h->ops.qr(h, a, st, h->S);  // per stream: exits unless due
     if (a.mask_out) {
       PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
@@ -851,7 +858,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   const char* kenv = getenv("PROST_KERNEL");
   std::string kpath = kenv ? kenv : (want_res && want_res[0] == '1' ? "resident" : "tmem");
   if (no_res && no_res[0] == '1') kpath = "streamed";
-  const bool eligible = !h->fp64 && h->C == 1 && K <= 20;
+  const bool eligible = !h->fp64 && K <= 20;
   const TmOps to = pick_tmem(K, params->p == 0.5);
   if (eligible && kpath == "tmem" && to.launch) {
     if (getenv("PROST_DEBUG")) to.describe();
@@ -863,7 +870,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
     // slot boundary costs a whole extra slot).  Depends on the stream shape
     // and the chip only (not on n_streams): per-stream results do not depend
     // on the batch.
-    const int nq = h->Pp / 4;
+    const int nq = (int)(h->np / 4);  // row groups over all channel planes
     int bestG = 0;
     double best_cost = 0;
     for (int G = 1; G <= sms; ++G) {
@@ -904,6 +911,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
         h->rG = G;
         h->rT = std::min(h->S, sms * TM_CPS / G);
         h->resident_ops_K = K;
+        if (h->C == 3) ALLOC(labc, S * np);
         ALLOC(rbar, (size_t)sms * TM_CPS * sizeof(unsigned));
         ALLOC(rpart, (size_t)2 * sms * TM_CPS * RES_RNV_MAX * sizeof(double));
         ALLOC(rprof, (size_t)sms * TM_CPS * PROF_N * sizeof(unsigned long long));
@@ -913,7 +921,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
     }
   }
   const ResOps ro = pick_resident(K, params->p == 0.5);
-  if (eligible && ro.launch && kpath == "resident") {
+  if (eligible && h->C == 1 && ro.launch && kpath == "resident") {
     const int nq = h->Pp / 4;
     int best_used = 0, best_qpc = 0;
     for (int qpc = ro.ntmax / 4 * 4; qpc >= 32; qpc -= 4) {
@@ -972,7 +980,7 @@ void prost_destroy(prost_handle* h) {
   if (!h) return;
   void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
                   h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage,
-                  h->rbar, h->rpart, h->rprof, h->xred, h->xgo};
+                  h->rbar, h->rpart, h->rprof, h->xred, h->xgo, h->labc};
   for (void* b : bufs)
     if (b) cudaFree(b);
   // pipelined-I/O slot buffers (slot 0's frame buffer is h->x's allocation,

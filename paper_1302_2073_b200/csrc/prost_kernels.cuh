@@ -107,6 +107,7 @@ struct Args {
   int* xgo;            // [S]
   const uint8_t* halo_top;  // [S][width] label row above the local rows, or null
   const uint8_t* halo_bot;  // [S][width] label row below the local rows, or null
+  uint8_t* labc;       // [S][np] per-coordinate flags of the TMEM kernel (3 channels), or null
   int s0;              // first stream of this launch
   int k, C, P, Pp, width, height;
   long long np;        // padded coordinates per stream = C * Pp

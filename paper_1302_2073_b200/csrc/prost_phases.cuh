@@ -835,6 +835,25 @@ __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) 
 }
 
 // ---------------------------------------------------------------------------
+// k_combine3: 3-channel label = any channel's abs(r') >= delta (pipeline.py:
+// 210-211) from the TMEM kernel's per-coordinate flags; streams whose frame
+// was rejected keep their labels.
+
+__global__ void __launch_bounds__(NT) k_combine3(const __grid_constant__ Args a) {
+  const int s = a.s0 + blockIdx.y;
+  if (a.ctl[s].status != ST_OK) return;
+  const uint32_t* F = reinterpret_cast<const uint32_t*>(a.labc + (size_t)s * a.np);
+  uint32_t* L = reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp);
+  uint32_t* R = a.raw_out ? reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp) : nullptr;
+  const int nw = a.Pp / 4, pw = a.Pp / 4;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < nw; q += gridDim.x * NT) {
+    const uint32_t v = F[q] | F[pw + q] | F[2 * pw + q];
+    L[q] = v;
+    if (R) R[q] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_xlogic: exchange mode — the scalar tail of phase `step` for every stream
 // the phase ran for, from the cross-rank sums in xred (one warp per stream).
 

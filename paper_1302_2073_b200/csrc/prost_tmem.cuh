@@ -148,7 +148,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int k = a.k;
-  const int nq = a.Pp / 4;
+  // row groups over the stream's stacked coordinates: with 3 channels a slice
+  // may cover parts of several planes (Pp is a multiple of 4: a row group never
+  // straddles two planes); labels and padding are per pixel
+  const int nq = (int)(a.np / 4);
   const int q0 = rank * qpc;
   const int qcount = max(0, min(qpc, nq - q0));
   const int nslots = (qcount + TM_NT - 1) / TM_NT;  // uniform across the CTA
@@ -217,9 +220,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   };
   const float omega = a.omegaf;
   // weights of a row group from the label words (layout without a weight column)
+  auto pixel_of = [&](int coord) { return a.C == 1 ? coord : coord % a.Pp; };
   auto lab_weights = [&](int qi, float (&w)[4]) {
     const uint32_t lb = qi < qcount ? sL[qi] : 0u;
-    const int pix = (q0 + qi) * 4;
+    const int pix = pixel_of((q0 + qi) * 4);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       w[e] = (qi < qcount && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
@@ -242,11 +246,11 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       for (int slot = 0; slot < nslots; ++slot) {
         const int qi = slot * TM_NT + tid;  // row group within the slice
         const bool ok = qi < qcount;
-        const int pix = (q0 + qi) * 4;
+        const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float4 p[K];
 #pragma unroll
         for (int j = 0; j < K; ++j)
-          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + pix)) : z4;
+          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + coord)) : z4;
         const uint32_t lb = ok ? *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + pix) : 0u;
         if (!WCOL) sL[qi] = lb;
 #pragma unroll
@@ -310,9 +314,9 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       for (int slot = 0; slot < nslots; ++slot) {
         const int qi = slot * TM_NT + tid;
         if (qi >= qcount) continue;
-        const int pix = (q0 + qi) * 4;
+        const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float xv[4];
-        f4(*reinterpret_cast<const float4*>(Xg + so + pix), xv);
+        f4(*reinterpret_cast<const float4*>(Xg + so + coord), xv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (pix + e < a.P) {
@@ -362,12 +366,12 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     const float stdv = (float)cs->std_cur, seen = (float)cs->pseen;
     auto xhat = [&](int qi, bool wr, float (&xh)[4], bool& bad) {
       const bool ok = qi < qcount;
-      const int pix = (q0 + qi) * 4;
+      const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
       float xv[4];
-      f4(ok ? *reinterpret_cast<const float4*>(Xg + so + pix) : z4, xv);
+      f4(ok ? *reinterpret_cast<const float4*>(Xg + so + coord) : z4, xv);
       if (a.pipeline) {
         float mv[4];
-        f4(ok ? *reinterpret_cast<const float4*>(Mg + so + pix) : z4, mv);
+        f4(ok ? *reinterpret_cast<const float4*>(Mg + so + coord) : z4, mv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           bad |= !isfinite(xv[e]);
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           if (pix + e >= a.P) xh[e] = 0.f;
         }
         if (wr && ok)
-          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + so + pix) =
+          *reinterpret_cast<float4*>(static_cast<float*>(a.mean) + so + coord) =
               make_float4(mv[0], mv[1], mv[2], mv[3]);
       } else {
 #pragma unroll
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
       sweep([&](int qi, const auto& rows) {
         const bool ok = qi < qcount;
-        const int pix = (q0 + qi) * 4;
+        const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float r[4], w[4], ud[4];
         f4(sR[qi], r);
         f4(sD[qi], ud);
@@ -652,11 +656,11 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #pragma unroll
           for (int j = 0; j < K; ++j)
             if (j < k)
-              __stcs(reinterpret_cast<float4*>(Ug + (size_t)j * a.np + pix),
+              __stcs(reinterpret_cast<float4*>(Ug + (size_t)j * a.np + coord),
                      make_float4(up[0][j], up[1][j], up[2][j], up[3][j]));
         }
         if (qr) return;
-        const size_t off = so + pix;
+        const size_t off = so + coord;
         // r' = x - U'y from the frame (tracker.py:146), as the reference orders it
         float xh[4], bgn[4];
         bool bad_unused = false;
@@ -668,8 +672,12 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           rr[e] = __fsub_rn(xh[e], bgn[e]);
           if (pix + e < a.P && fabsf(rr[e]) >= a.delta) nl |= 1u << (8 * e);
         }
-        *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
-        if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
+        if (a.C == 1) {
+          *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
+          if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
+        } else {  // per-channel flags; k_combine3 takes the max over channels (pipeline.py:210-211)
+          *reinterpret_cast<uint32_t*>(a.labc + off) = nl;
+        }
         if (a.res_out)
           *reinterpret_cast<float4*>(static_cast<float*>(a.res_out) + off) = make_float4(rr[0], rr[1], rr[2], rr[3]);
         if (a.bg_out) {

@@ -344,6 +344,37 @@ def test_tmem_k20_matches_streamed(monkeypatch):
     assert np.linalg.norm(b1 - b2) <= 1e-5 * np.linalg.norm(b2)
 
 
+def test_tmem_rgb_matches_streamed(monkeypatch):
+    """Three channel planes (BASELINE C1) on the TMEM kernel: slices span the
+    stacked planes, per-channel threshold flags are combined into the per-pixel
+    label (pipeline.py:210-211) and the 3-channel weight expansion
+    (jobs.py:218-221); agrees with the streamed kernels."""
+    import torch
+    from paper_1302_2073_b200 import _native as nat
+    from paper_1302_2073_b200.synth import SceneSpec, SceneStream
+
+    W, H, S, F = 96, 64, 2, 9
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=False, i_init=4, seed=0)
+    data = [SceneStream(SceneSpec(width=W, height=H, channels=3, rank=6, n_objects=(2, 3),
+                                  shape="ellipse", seed=s)).next_frames(F) for s in range(S)]
+    out = {}
+    for path, code in (("tmem", 2), ("streamed", 0)):
+        monkeypatch.setenv("PROST_KERNEL", path)
+        bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        assert bt.native.query(nat.Q_RESIDENT) == code
+        mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        raw = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((S, 3 * W * H), dtype=torch.float32, device="cuda")
+        for f in range(F):
+            fr = torch.from_numpy(np.stack([d[f] for d in data]).astype(np.float32)).cuda()
+            bt.push(fr, background=bg, mask=mask, raw_mask=raw)
+        out[path] = (mask.cpu().numpy(), raw.cpu().numpy(), bg.cpu().numpy())
+    (m1, r1, b1), (m2, r2, b2) = out["tmem"], out["streamed"]
+    assert np.mean(r1 != r2) <= 0.001 and np.mean(m1 != m2) <= 0.001
+    assert np.linalg.norm(b1 - b2) <= 1e-5 * np.linalg.norm(b2)
+
+
 @pytest.mark.parametrize("mode", ["tmem", "resident"])
 def test_resident_kernels_match_streamed(mode, monkeypatch):
     """The TMEM-resident (default for fp32 single-channel streams) and the
