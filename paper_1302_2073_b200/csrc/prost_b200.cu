@@ -232,7 +232,12 @@ struct PhaseTimer {
 
 // 3x3 majority filter of the raw labels into a.mask_out (pipeline.py:215-228)
 void launch_median(prost_handle* h, const Args& a, cudaStream_t st, int sw) {
-  if (h->prm.width % 4 == 0 && ((uintptr_t)a.mask_out & 3) == 0) {
+  const uintptr_t al = (uintptr_t)a.mask_out | (uintptr_t)a.halo_top | (uintptr_t)a.halo_bot;
+  if (h->prm.width % 16 == 0 && (al & 15) == 0 && h->Pp % 16 == 0) {
+    const int nw = h->P / 16;
+    const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
+    k_median16<<<mg, NT, 0, st>>>(a);
+  } else if (h->prm.width % 4 == 0 && ((uintptr_t)a.mask_out & 3) == 0) {
     const int nw = h->P / 4;
     const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
     k_median4<<<mg, NT, 0, st>>>(a);

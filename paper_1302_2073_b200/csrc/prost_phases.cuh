@@ -834,6 +834,41 @@ __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) 
   }
 }
 
+// k_median16: sixteen pixels per thread (widths that are a multiple of 16):
+// three 16-byte row loads and two edge bytes per row per 16 pixels.
+__global__ void __launch_bounds__(NT) k_median16(const __grid_constant__ Args a) {
+  const int s = a.s0 + blockIdx.y;
+  if (a.ctl[s].status != ST_OK) return;
+  const int W = a.width, H = a.height, wq = W >> 4;
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  uint8_t* M = a.mask_out + (size_t)s * a.Pp;
+  const uint8_t* above = a.halo_top ? a.halo_top + (size_t)s * W : L;
+  const uint8_t* below = a.halo_bot ? a.halo_bot + (size_t)s * W : L + (size_t)(H - 1) * W;
+  const int nw = wq * H;
+  for (int q = blockIdx.x * NT + threadIdx.x; q < nw; q += gridDim.x * NT) {
+    const int yy = q / wq, x0 = (q - yy * wq) << 4;
+    const int xl = x0 > 0 ? x0 - 1 : 0, xr = x0 + 16 < W ? x0 + 16 : W - 1;
+    const uint8_t* ra = yy > 0 ? L + (size_t)(yy - 1) * W : above;
+    const uint8_t* rm = L + (size_t)yy * W;
+    const uint8_t* rb = yy < H - 1 ? L + (size_t)(yy + 1) * W : below;
+    const uint4 A = __ldg(reinterpret_cast<const uint4*>(ra + x0));
+    const uint4 B = __ldg(reinterpret_cast<const uint4*>(rm + x0));
+    const uint4 C = __ldg(reinterpret_cast<const uint4*>(rb + x0));
+    const uint32_t v[4] = {A.x + B.x + C.x, A.y + B.y + C.y, A.z + B.z + C.z, A.w + B.w + C.w};
+    const uint32_t l = (uint32_t)__ldg(ra + xl) + __ldg(rm + xl) + __ldg(rb + xl);
+    const uint32_t r = (uint32_t)__ldg(ra + xr) + __ldg(rm + xr) + __ldg(rb + xr);
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t lb = i > 0 ? (v[i - 1] >> 24) : l;
+      const uint32_t rb8 = i < 3 ? (v[i + 1] & 0xffu) : r;
+      const uint32_t win = v[i] + ((v[i] << 8) | lb) + ((v[i] >> 8) | (rb8 << 24));
+      o[i] = __vcmpgeu4(win, 0x05050505u) & 0x01010101u;
+    }
+    *reinterpret_cast<uint4*>(M + (size_t)yy * W + x0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // k_combine3: 3-channel label = any channel's abs(r') >= delta (pipeline.py:
 // 210-211) from the TMEM kernel's per-coordinate flags; streams whose frame
