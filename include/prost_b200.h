@@ -186,6 +186,17 @@ int prost_profile_read(prost_handle* h, double* ms, int64_t* launches, int32_t n
 /* Tuning knob: streams per launch wave (0 = automatic, sized to L2). */
 int prost_set_wave(prost_handle* h, int32_t streams_per_wave);
 
+/* ---- Resampling shell -------------------------------
+ * Device buffers, enqueued on cuda_stream; no handle.
+ *   prost_resample: bilinear, half-pixel centres, per channel plane
+ *     (resample, pipeline.py:164-193); u8 input is divided by 255 first.
+ *   prost_upsample_mask: nearest neighbour on categorical labels
+ *     (upsample_mask, pipeline.py:245-258). */
+int prost_resample(const void* src, int32_t dtype_in, int32_t channels, int32_t w_in, int32_t h_in,
+                   void* dst, int32_t dtype_out, int32_t w_out, int32_t h_out, void* cuda_stream);
+int prost_upsample_mask(const uint8_t* src, int32_t w_in, int32_t h_in, uint8_t* dst, int32_t w_out,
+                        int32_t h_out, void* cuda_stream);
+
 /* ---- Exchange (pixel-sharded) mode, SURVEY.md §8(e) ------------------------
  * One stream too large for one GPU (BASELINE config C4) is split by image
  * rows: rank g's handle is created for its block of rows (params.height =

@@ -361,3 +361,41 @@ def subspace_sine(A: np.ndarray, B: np.ndarray) -> float:
     """Sine of the largest principal angle (evaluate.py:207-218)."""
     off = B - A @ (A.T @ B)
     return float(np.linalg.svd(off, compute_uv=False)[0])
+
+
+# --------------------------------------------------------------------------
+# Resampling shell (pipeline.py:164-193, 245-258)
+
+
+def resample_planes(data: np.ndarray, channels: int, width: int, height: int, out_w: int,
+                    out_h: int) -> np.ndarray:
+    """pipeline.py:164-193: bilinear per plane, half-pixel centres, clipped
+    source coordinates; identity sizes return the data unchanged."""
+    if (out_w, out_h) == (width, height):
+        return data
+
+    def axis(n_out, n_in):
+        src = (np.arange(n_out) + 0.5) * (n_in / n_out) - 0.5
+        src = np.clip(src, 0.0, n_in - 1.0)
+        lo = np.floor(src).astype(int)
+        return lo, np.minimum(lo + 1, n_in - 1), src - lo
+
+    x0, x1, wx = axis(out_w, width)
+    y0, y1, wy = axis(out_h, height)
+    wx = wx[None, :]
+    wy = wy[:, None]
+    out = []
+    for plane in data.reshape(channels, height, width):
+        top = (1.0 - wx) * plane[np.ix_(y0, x0)] + wx * plane[np.ix_(y0, x1)]
+        bottom = (1.0 - wx) * plane[np.ix_(y1, x0)] + wx * plane[np.ix_(y1, x1)]
+        out.append(((1.0 - wy) * top + wy * bottom).reshape(-1))
+    return np.concatenate(out)
+
+
+def upsample_labels(labels: np.ndarray, width: int, height: int, out_w: int, out_h: int) -> np.ndarray:
+    """pipeline.py:245-258: nearest neighbour on categorical labels."""
+    if (out_w, out_h) == (width, height):
+        return labels
+    xs = np.minimum(((np.arange(out_w) + 0.5) * (width / out_w)).astype(int), width - 1)
+    ys = np.minimum(((np.arange(out_h) + 0.5) * (height / out_h)).astype(int), height - 1)
+    return labels.reshape(height, width)[np.ix_(ys, xs)].reshape(-1)

@@ -1348,6 +1348,39 @@ int prost_join(prost_handle* h, void* cuda_stream) {
   return PROST_OK;
 }
 
+// Resampling shell: device buffers, no handle (pipeline.py:164-193, 245-258).
+int prost_resample(const void* src, int32_t dtype_in, int32_t channels, int32_t w_in, int32_t h_in,
+                   void* dst, int32_t dtype_out, int32_t w_out, int32_t h_out, void* cuda_stream) {
+  if (!src || !dst) return PROST_ERR_DIMENSION;
+  if (w_in < 1 || h_in < 1 || w_out < 1 || h_out < 1 || (channels != 1 && channels != 3))
+    return PROST_ERR_DIMENSION;
+  if (dtype_out == PROST_U8) return PROST_ERR_CONFIG;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const long long total = (long long)channels * w_out * h_out;
+  const int nb = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  const double sc = dtype_in == PROST_U8 ? 1.0 / 255.0 : 1.0;
+#define RS_LAUNCH(TI, TO) \
+  k_resample<TI, TO><<<nb, 256, 0, st>>>((const TI*)src, (TO*)dst, channels, w_in, h_in, w_out, h_out, sc)
+  if (dtype_in == PROST_F64 && dtype_out == PROST_F64) RS_LAUNCH(double, double);
+  else if (dtype_in == PROST_F64) RS_LAUNCH(double, float);
+  else if (dtype_in == PROST_F32 && dtype_out == PROST_F64) RS_LAUNCH(float, double);
+  else if (dtype_in == PROST_F32) RS_LAUNCH(float, float);
+  else if (dtype_out == PROST_F64) RS_LAUNCH(uint8_t, double);
+  else RS_LAUNCH(uint8_t, float);
+#undef RS_LAUNCH
+  return cudaGetLastError() == cudaSuccess ? PROST_OK : PROST_ERR_CUDA;
+}
+
+int prost_upsample_mask(const uint8_t* src, int32_t w_in, int32_t h_in, uint8_t* dst, int32_t w_out,
+                        int32_t h_out, void* cuda_stream) {
+  if (!src || !dst) return PROST_ERR_DIMENSION;
+  if (w_in < 1 || h_in < 1 || w_out < 1 || h_out < 1) return PROST_ERR_DIMENSION;
+  const long long total = (long long)w_out * h_out;
+  const int nb = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  k_upsample_mask<<<nb, 256, 0, (cudaStream_t)cuda_stream>>>(src, dst, w_in, h_in, w_out, h_out);
+  return cudaGetLastError() == cudaSuccess ? PROST_OK : PROST_ERR_CUDA;
+}
+
 int prost_synchronize(prost_handle* h) {
   if (!h) return PROST_ERR_CONFIG;
   CK(cudaSetDevice(h->device));

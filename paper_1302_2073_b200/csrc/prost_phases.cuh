@@ -870,6 +870,55 @@ __global__ void __launch_bounds__(NT) k_median16(const __grid_constant__ Args a)
 }
 
 // ---------------------------------------------------------------------------
+// Resampling shell: bilinear frame resampling with
+// half-pixel centres (pipeline.py:164-193) and nearest-neighbour mask
+// upsampling (pipeline.py:245-258), in fp64 with the reference's operation
+// order and no FMA contraction, so results equal numpy's bit for bit.
+
+__device__ __forceinline__ void axis_coord(int i, int n_out, int n_in, int& lo, int& hi, double& w) {
+  double src = __dsub_rn(__dmul_rn((double)i + 0.5, (double)n_in / (double)n_out), 0.5);
+  src = fmin(fmax(src, 0.0), (double)n_in - 1.0);
+  lo = (int)floor(src);
+  hi = min(lo + 1, n_in - 1);
+  w = __dsub_rn(src, (double)lo);
+}
+
+template <typename TI, typename TO>
+__global__ void k_resample(const TI* __restrict__ src, TO* __restrict__ dst, int C, int w_in,
+                           int h_in, int w_out, int h_out, double scale) {
+  const long long total = (long long)C * w_out * h_out;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ((long long)w_out * h_out));
+    const int rem = (int)(i - (long long)c * w_out * h_out);
+    const int oy = rem / w_out, ox = rem - oy * w_out;
+    int x0, x1, y0, y1;
+    double wx, wy;
+    axis_coord(ox, w_out, w_in, x0, x1, wx);
+    axis_coord(oy, h_out, h_in, y0, y1, wy);
+    const TI* pl = src + (size_t)c * w_in * h_in;
+    const double a00 = (double)pl[(size_t)y0 * w_in + x0] * scale, a01 = (double)pl[(size_t)y0 * w_in + x1] * scale;
+    const double a10 = (double)pl[(size_t)y1 * w_in + x0] * scale, a11 = (double)pl[(size_t)y1 * w_in + x1] * scale;
+    const double top = __dadd_rn(__dmul_rn(1.0 - wx, a00), __dmul_rn(wx, a01));
+    const double bot = __dadd_rn(__dmul_rn(1.0 - wx, a10), __dmul_rn(wx, a11));
+    dst[i] = (TO)__dadd_rn(__dmul_rn(1.0 - wy, top), __dmul_rn(wy, bot));
+  }
+}
+
+__global__ void k_upsample_mask(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int w_in,
+                                int h_in, int w_out, int h_out) {
+  const long long total = (long long)w_out * h_out;
+  const double fx = (double)w_in / (double)w_out, fy = (double)h_in / (double)h_out;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int oy = (int)(i / w_out), ox = (int)(i - (long long)oy * w_out);
+    const int xs = min((int)__dmul_rn((double)ox + 0.5, fx), w_in - 1);
+    const int ys = min((int)__dmul_rn((double)oy + 0.5, fy), h_in - 1);
+    dst[i] = src[(size_t)ys * w_in + xs];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_combine3: 3-channel label = any channel's abs(r') >= delta (pipeline.py:
 // 210-211) from the TMEM kernel's per-coordinate flags; streams whose frame
 // was rejected keep their labels.

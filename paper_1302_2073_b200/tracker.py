@@ -478,13 +478,15 @@ class StreamTracker:
         return self._frame_index
 
     def _prepare(self, frame: FrameBuffer) -> FrameBuffer:
+        # jobs.py:181-184: gray conversion, then bilinear resampling to the
+        # model resolution (on the device, resample.py; identity sizes pass)
         if self.config.grayscale:
             frame = frame.to_gray()
         if (frame.width, frame.height) != (self.config.target_width, self.config.target_height):
-            raise DimensionError(
-                f"frame is {frame.width}x{frame.height}; this build processes frames at model "
-                f"resolution {self.config.target_width}x{self.config.target_height} "
-                "(resampling is outside the device path)")
+            from .resample import resample
+
+            frame = resample(frame, self.config.target_width, self.config.target_height,
+                             device=self.device)
         return frame
 
     def _start(self, channels: int) -> None:

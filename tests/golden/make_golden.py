@@ -163,6 +163,26 @@ def snapshot_run(n_before=8, n_after=6, i_init=5):
          cfg=np.array([4, 0.5, 1e-4, 2, i_init, 4, n_before]))
 
 
+def resample_vectors():
+    """pipeline.py:164-193 and 245-258 of the reference on seeded inputs."""
+    from prost.pipeline import SegmentationMask, resample, upsample_mask
+
+    rng = np.random.default_rng(17)
+    keep = {}
+    cases = [(1, 37, 23, 16, 12), (3, 20, 15, 33, 27), (1, 40, 30, 80, 60), (3, 64, 48, 32, 24)]
+    for i, (c, w, h, ow, oh) in enumerate(cases):
+        data = rng.random(c * w * h)
+        out = resample(FrameBuffer(w, h, c, data), ow, oh)
+        keep[f"in{i}"] = data
+        keep[f"out{i}"] = out.data
+        keep[f"dims{i}"] = np.array([c, w, h, ow, oh])
+        lab = (rng.random(w * h) < 0.3).astype(np.uint8)
+        up = upsample_mask(SegmentationMask(w, h, lab), ow, oh)
+        keep[f"lab{i}"] = lab
+        keep[f"up{i}"] = up.labels
+    save("resample_vectors", **keep)
+
+
 if __name__ == "__main__":
     print("reference prost", prost.__version__, "numpy", np.__version__)
     cost_vectors()
@@ -172,3 +192,4 @@ if __name__ == "__main__":
     push_run("push_gray", 1)
     push_run("push_rgb", 3)
     snapshot_run()
+    resample_vectors()
