@@ -197,6 +197,13 @@ int prost_resample(const void* src, int32_t dtype_in, int32_t channels, int32_t 
 int prost_upsample_mask(const uint8_t* src, int32_t w_in, int32_t h_in, uint8_t* dst, int32_t w_out,
                         int32_t h_out, void* cuda_stream);
 
+/* Confusion counts of predicted masks against ground-truth frames
+ * (accumulate, evaluate.py:87-106): counts[S][4] =
+ * {tp, fp, tn, fn} (int64, device) are incremented; ground-truth gray levels
+ * 85 (outside ROI) and 170 (unknown) are not scored, 255 is foreground. */
+int prost_confusion(const uint8_t* mask, int64_t mask_stride, const uint8_t* truth, int32_t n_streams,
+                    int32_t pixels, int64_t* counts, void* cuda_stream);
+
 /* ---- Exchange (pixel-sharded) mode, SURVEY.md §8(e) ------------------------
  * One stream too large for one GPU (BASELINE config C4) is split by image
  * rows: rank g's handle is created for its block of rows (params.height =

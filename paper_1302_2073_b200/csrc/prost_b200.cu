@@ -1381,6 +1381,19 @@ int prost_upsample_mask(const uint8_t* src, int32_t w_in, int32_t h_in, uint8_t*
   return cudaGetLastError() == cudaSuccess ? PROST_OK : PROST_ERR_CUDA;
 }
 
+// Confusion counts (evaluate.py:87-106), accumulated into counts[S][4] =
+// {tp, fp, tn, fn} (int64, device).  mask: [S] rows of mask_stride bytes
+// (>= pixels; a handle's padded masks or dense ones), truth: dense [S][pixels].
+int prost_confusion(const uint8_t* mask, int64_t mask_stride, const uint8_t* truth, int32_t n_streams,
+                    int32_t pixels, int64_t* counts, void* cuda_stream) {
+  if (!mask || !truth || !counts) return PROST_ERR_DIMENSION;
+  if (n_streams < 1 || pixels < 1 || mask_stride < pixels) return PROST_ERR_DIMENSION;
+  const dim3 grid(std::max(1, std::min((pixels + NT - 1) / NT, 64)), n_streams);
+  k_confusion<<<grid, NT, 0, (cudaStream_t)cuda_stream>>>(mask, truth, pixels, mask_stride,
+                                                         (unsigned long long*)counts);
+  return cudaGetLastError() == cudaSuccess ? PROST_OK : PROST_ERR_CUDA;
+}
+
 int prost_synchronize(prost_handle* h) {
   if (!h) return PROST_ERR_CONFIG;
   CK(cudaSetDevice(h->device));

@@ -919,6 +919,39 @@ __global__ void k_upsample_mask(const uint8_t* __restrict__ src, uint8_t* __rest
 }
 
 // ---------------------------------------------------------------------------
+// k_confusion: per-stream tp / fp / tn / fn of a predicted mask against a
+// ground-truth frame (evaluate.py:87-106): pixels labelled outside-ROI (85) or
+// unknown (170) are not scored, 255 is foreground, every other value
+// background.  Integer atomics: exact and order-independent.
+
+__global__ void __launch_bounds__(NT) k_confusion(const uint8_t* __restrict__ mask,
+                                                  const uint8_t* __restrict__ truth, int P,
+                                                  long long mask_stride, unsigned long long* counts) {
+  const int s = blockIdx.y;
+  const uint8_t* M = mask + (size_t)s * mask_stride;
+  const uint8_t* G = truth + (size_t)s * P;
+  unsigned c[4] = {0u, 0u, 0u, 0u};  // tp, fp, tn, fn
+  for (int p = blockIdx.x * NT + threadIdx.x; p < P; p += gridDim.x * NT) {
+    const unsigned g = G[p];
+    if (g == 85u || g == 170u) continue;
+    const bool tfg = g == 255u, pfg = M[p] != 0;
+    c[tfg ? (pfg ? 0 : 3) : (pfg ? 1 : 2)] += 1u;
+  }
+  __shared__ unsigned long long sc[4];
+  if (threadIdx.x < 4) sc[threadIdx.x] = 0ull;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    unsigned v = c[i];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sc[i], (unsigned long long)v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && sc[threadIdx.x]) atomicAdd(counts + (size_t)s * 4 + threadIdx.x, sc[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
 // k_combine3: 3-channel label = any channel's abs(r') >= delta (pipeline.py:
 // 210-211) from the TMEM kernel's per-coordinate flags; streams whose frame
 // was rejected keep their labels.

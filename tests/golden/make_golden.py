@@ -183,6 +183,26 @@ def resample_vectors():
     save("resample_vectors", **keep)
 
 
+def confusion_vectors():
+    """evaluate.py:87-106 of the reference on seeded masks and ground truth."""
+    from prost.evaluate import ConfusionCounts, accumulate
+    from prost.frameio import GroundTruthFrame
+    from prost.pipeline import SegmentationMask
+
+    rng = np.random.default_rng(23)
+    keep = {}
+    levels = np.array([0, 50, 85, 170, 255], dtype=np.uint8)
+    for i, (w, h) in enumerate([(32, 24), (160, 120), (7, 5)]):
+        lab = (rng.random(w * h) < 0.3).astype(np.uint8)
+        gt = levels[rng.integers(0, 5, size=w * h)]
+        c = accumulate(ConfusionCounts(), SegmentationMask(w, h, lab), GroundTruthFrame(w, h, gt))
+        keep[f"mask{i}"] = lab
+        keep[f"gt{i}"] = gt
+        keep[f"dims{i}"] = np.array([w, h])
+        keep[f"counts{i}"] = np.array([c.tp, c.fp, c.tn, c.fn])
+    save("confusion_vectors", **keep)
+
+
 if __name__ == "__main__":
     print("reference prost", prost.__version__, "numpy", np.__version__)
     cost_vectors()
@@ -193,3 +213,4 @@ if __name__ == "__main__":
     push_run("push_rgb", 3)
     snapshot_run()
     resample_vectors()
+    confusion_vectors()
