@@ -198,15 +198,16 @@ def test_stream_tracker_rejects_bad_input():
     tr.push(pkg.FrameBuffer(16, 8, 1, rng.random(128)))
     with pytest.raises(pkg.SequenceError):  # jobs.py:195-198
         tr.push(pkg.FrameBuffer(16, 8, 3, rng.random(384)))
-    with pytest.raises(pkg.DimensionError):
-        tr.push(pkg.FrameBuffer(8, 8, 1, rng.random(64)))
+    # an off-resolution frame is resampled to the model resolution (jobs.py:181-184)
+    rec = tr.push(pkg.FrameBuffer(8, 8, 1, rng.random(64)))
+    assert rec.frame_index == 2 and rec.mask.width == 16 and rec.mask.height == 8
     bad = rng.random(128)
     bad[3] = np.inf
     with pytest.raises(pkg.NonFiniteError):
         tr.push(pkg.FrameBuffer(16, 8, 1, bad))
-    assert tr.frame_index == 1
+    assert tr.frame_index == 2
     rec = tr.push(pkg.FrameBuffer(16, 8, 1, rng.random(128)))
-    assert rec.frame_index == 2
+    assert rec.frame_index == 3
 
 
 # ---------------------------------------------------------------------------
