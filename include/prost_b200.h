@@ -197,6 +197,11 @@ int prost_resample(const void* src, int32_t dtype_in, int32_t channels, int32_t 
 int prost_upsample_mask(const uint8_t* src, int32_t w_in, int32_t h_in, uint8_t* dst, int32_t w_out,
                         int32_t h_out, void* cuda_stream);
 
+/* Binary PGM / PPM payload (after the header, parsed on the host) to a
+ * channel-planar frame on [0, 1] (decode_pnm, frameio.py:120-137). */
+int prost_unpack_pnm(const uint8_t* payload, int32_t channels, int32_t pixels, void* dst,
+                     int32_t dtype_out, void* cuda_stream);
+
 /* Confusion counts of predicted masks against ground-truth frames
  * (accumulate, evaluate.py:87-106): counts[S][4] =
  * {tp, fp, tn, fn} (int64, device) are incremented; ground-truth gray levels

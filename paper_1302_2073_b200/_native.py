@@ -30,7 +30,7 @@ EXPORTS = (
     "prost_set_wave", "prost_profile", "prost_profile_read", "prost_resident_counters",
     "prost_set_exchange", "prost_xbuffer", "prost_xbegin", "prost_xnext", "prost_xapply",
     "prost_xedges", "prost_xfinish", "prost_join", "prost_resample", "prost_upsample_mask",
-    "prost_confusion",
+    "prost_confusion", "prost_unpack_pnm",
 )
 PHASES = ("stats", "cold", "pass0", "iter", "lsfb", "gradfb", "geo", "qr", "median", "frame")
 
@@ -118,6 +118,7 @@ def lib() -> ctypes.CDLL:
     L.prost_resample.argtypes = [vp, i32, i32, i32, i32, vp, i32, i32, i32, vp]
     L.prost_upsample_mask.argtypes = [vp, i32, i32, vp, i32, i32, vp]
     L.prost_confusion.argtypes = [vp, i64, vp, i32, i32, vp, vp]
+    L.prost_unpack_pnm.argtypes = [vp, i32, i32, vp, i32, vp]
     for name in EXPORTS:
         if name not in ("prost_destroy",):
             getattr(L, name).restype = ctypes.c_int

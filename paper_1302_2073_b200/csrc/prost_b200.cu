@@ -1394,6 +1394,20 @@ int prost_confusion(const uint8_t* mask, int64_t mask_stride, const uint8_t* tru
   return cudaGetLastError() == cudaSuccess ? PROST_OK : PROST_ERR_CUDA;
 }
 
+// Netpbm payload unpack (frameio.py:120-137): device payload of pixels x
+// channels interleaved bytes -> planar f32 / f64 on [0, 1].
+int prost_unpack_pnm(const uint8_t* payload, int32_t channels, int32_t pixels, void* dst,
+                     int32_t dtype_out, void* cuda_stream) {
+  if (!payload || !dst || pixels < 1 || (channels != 1 && channels != 3)) return PROST_ERR_DIMENSION;
+  if (dtype_out != PROST_F32 && dtype_out != PROST_F64) return PROST_ERR_CONFIG;
+  const long long total = (long long)channels * pixels;
+  const int nb = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (dtype_out == PROST_F64) k_unpack_pnm<double><<<nb, 256, 0, st>>>(payload, channels, pixels, (double*)dst);
+  else k_unpack_pnm<float><<<nb, 256, 0, st>>>(payload, channels, pixels, (float*)dst);
+  return cudaGetLastError() == cudaSuccess ? PROST_OK : PROST_ERR_CUDA;
+}
+
 int prost_synchronize(prost_handle* h) {
   if (!h) return PROST_ERR_CONFIG;
   CK(cudaSetDevice(h->device));

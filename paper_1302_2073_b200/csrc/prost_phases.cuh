@@ -952,6 +952,21 @@ __global__ void __launch_bounds__(NT) k_confusion(const uint8_t* __restrict__ ma
 }
 
 // ---------------------------------------------------------------------------
+// k_unpack_pnm: binary PGM / PPM payload (interleaved u8) -> channel-planar
+// intensities on [0, 1] (decode_pnm, frameio.py:120-137): x / 255 in fp64
+// (correctly rounded, as numpy), then the output type.
+
+template <typename TO>
+__global__ void k_unpack_pnm(const uint8_t* __restrict__ payload, int C, int P, TO* __restrict__ dst) {
+  const long long total = (long long)C * P;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / P), p = (int)(i - (long long)c * P);
+    dst[i] = (TO)__ddiv_rn((double)payload[(size_t)p * C + c], 255.0);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_combine3: 3-channel label = any channel's abs(r') >= delta (pipeline.py:
 // 210-211) from the TMEM kernel's per-coordinate flags; streams whose frame
 // was rejected keep their labels.

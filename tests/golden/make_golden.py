@@ -203,6 +203,24 @@ def confusion_vectors():
     save("confusion_vectors", **keep)
 
 
+def pnm_vectors():
+    """frameio.decode_pnm of the reference on P5 / P6 bytes with varied headers."""
+    from prost.frameio import decode_pnm
+
+    rng = np.random.default_rng(29)
+    keep = {}
+    specs = [(b"P5", 7, 5, b"P5\n7 5\n255\n"), (b"P6", 6, 4, b"P6 6\t4 255\n"),
+             (b"P6", 33, 17, b"P6\n  33   17\n255 ")]
+    for i, (magic, w, h, header) in enumerate(specs):
+        c = 1 if magic == b"P5" else 3
+        blob = header + rng.integers(0, 256, size=w * h * c, dtype=np.uint8).tobytes() + b"tail"
+        fb = decode_pnm(blob)
+        keep[f"blob{i}"] = np.frombuffer(blob, dtype=np.uint8)
+        keep[f"data{i}"] = fb.data
+        keep[f"dims{i}"] = np.array([fb.width, fb.height, fb.channels])
+    save("pnm_vectors", **keep)
+
+
 if __name__ == "__main__":
     print("reference prost", prost.__version__, "numpy", np.__version__)
     cost_vectors()
@@ -214,3 +232,4 @@ if __name__ == "__main__":
     snapshot_run()
     resample_vectors()
     confusion_vectors()
+    pnm_vectors()
