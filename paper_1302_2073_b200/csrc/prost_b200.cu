@@ -589,7 +589,7 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   // device (one small synchronous read every ~QR_EVERY frames).
   if (h->qr_bound >= QR_EVERY - 1) {
     std::vector<Ctl> cs(h->S);
-    CK(cudaStreamSynchronize(st));
+    CK(cudaDeviceSynchronize());  // every stream (also the pipelined-I/O ones) is done with ctl
     CK(cudaMemcpy(cs.data(), h->ctl, (size_t)h->S * sizeof(Ctl), cudaMemcpyDeviceToHost));
     long long mx = 0;
     for (const Ctl& c : cs) mx = std::max(mx, c.since_qr);
@@ -1167,7 +1167,10 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   Args a;
   prost_outputs o{};
   const char* nopipe = getenv("PROST_NO_PIPE");
-  if (!on_device && out && !out->on_device && !out->fit && !h->prof && !(nopipe && nopipe[0] == '1'))
+  // (raw labels are copied from the label state itself, which the next frame's
+  // kernels overwrite: no pipelining when they are requested)
+  if (!on_device && out && !out->on_device && !out->fit && !out->raw_mask && !h->prof &&
+      !(nopipe && nopipe[0] == '1'))
     return push_pipelined(h, frames, dtype, out, st);
   if (h->io_pending) {  // order after the pipelined pushes before this one
     CK(cudaStreamWaitEvent(st, h->ev_comp[h->io_last], 0));
