@@ -35,6 +35,9 @@
 #ifndef PROST_TM_CPS
 #define PROST_TM_CPS 1
 #endif
+#ifndef PROST_RCP_STD
+#define PROST_RCP_STD 1  // normalize with the reciprocal of the std (<= 1 ulp from x / std)
+#endif
 
 
 namespace prost {
@@ -364,6 +367,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     // normalized frame of a row group (pipeline.py:148-156); the sweep that
     // owns this frame's running-mean update writes the mean back
     const float stdv = (float)cs->std_cur, seen = (float)cs->pseen;
+    const float inv_std = (float)(1.0 / cs->std_cur);
     auto xhat = [&](int qi, bool wr, float (&xh)[4], bool& bad) {
       const bool ok = qi < qcount;
       const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
@@ -376,7 +380,11 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         for (int e = 0; e < 4; ++e) {
           bad |= !isfinite(xv[e]);
           if (wr) mv[e] = __fadd_rn(mv[e], __fdiv_rn(__fsub_rn(xv[e], mv[e]), seen));
+#if PROST_RCP_STD
+          xh[e] = __fmul_rn(__fsub_rn(xv[e], mv[e]), inv_std);
+#else
           xh[e] = __fdiv_rn(__fsub_rn(xv[e], mv[e]), stdv);
+#endif
           if (pix + e >= a.P) xh[e] = 0.f;
         }
         if (wr && ok)
