@@ -629,7 +629,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       // unlabeled; the streamed k_gram / k_geo<QR> kernels that follow the
       // launch apply U' R^-1 and relabel (manifold.py:192-196).
       const bool geo = cs->do_geo != 0, qr = geo && cs->qr_now != 0;
-      const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s, ln = (float)cs->geo_ln;
+      const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s;
+      const float inv_ln = geo ? (float)(1.0 / cs->geo_ln) : 0.f;  // s = pi(eta) / ||pi(eta)||
       const float pa = (float)cs->pend_alpha;
       float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
       sweep([&](int qi, const auto& rows) {
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             const float eta = -g;  // cost.py:103-112
             const float uv = dotk<K>(u, sfv[2]);
             const float ug = dotk<K>(u, sfv[3]);
-            coef = ga * uv - gsn * ((eta - ug) / ln);
+            coef = ga * uv - gsn * ((eta - ug) * inv_ln);
           }
 #pragma unroll
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
