@@ -195,6 +195,8 @@ Args make_args(prost_handle* h, int s0) {
   a.half_pf = (float)a.half_p;
   a.muf = (float)a.mu;
   a.omegaf = (float)a.omega;
+  a.deltaf = (float)a.delta;
+  if ((double)a.deltaf < a.delta) a.deltaf = std::nextafter(a.deltaf, INFINITY);
   return a;
 }
 

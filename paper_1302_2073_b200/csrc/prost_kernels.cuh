@@ -115,6 +115,7 @@ struct Args {
   int pipeline, max_iters, max_bt, i_init, pmode, n_real;
   double p, half_p, mu, delta, omega, t_init, t_min, tau, grad_tol, step0, shrink, c_armijo;
   float pf, half_pf, muf, omegaf;  // fp32 copies for the per-element math
+  float deltaf;  // smallest float >= delta: abs(r) >= deltaf <=> (double)abs(r) >= delta
 };
 
 // ---------------------------------------------------------------------------

@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         for (int e = 0; e < 4; ++e) {
           bgn[e] = dotk<K>(up[e], sfv[0]);
           rr[e] = __fsub_rn(xh[e], bgn[e]);
-          if (pix + e < a.P && fabsf(rr[e]) >= a.delta) nl |= 1u << (8 * e);
+          if (pix + e < a.P && fabsf(rr[e]) >= a.deltaf) nl |= 1u << (8 * e);
         }
         if (a.C == 1) {
           *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
