@@ -123,6 +123,11 @@ class Fit:
     iterations: int
     cost_evals: int
     grad_evals: int
+    # parity-protocol instrumentation (not part of the reference's FitResult):
+    # the smallest relative distance |cost - rhs| / |f| of any Armijo test of
+    # this fit.  A second implementation whose cost differs from the
+    # reference's by more than this may legitimately take the other branch.
+    armijo_margin: float = float("inf")
 
 
 def fit(U: np.ndarray, x: np.ndarray, y0, prm: OracleParams, w=None) -> Fit:
@@ -145,6 +150,7 @@ def fit(U: np.ndarray, x: np.ndarray, y0, prm: OracleParams, w=None) -> Fit:
     f, gr = value_and_coord_grad(res)
     d = -gr
     done_iters = 0
+    margin = float("inf")
     for it in range(prm.max_iters):
         gnorm = float(np.linalg.norm(gr))
         if gnorm <= prm.grad_tol:
@@ -161,7 +167,10 @@ def fit(U: np.ndarray, x: np.ndarray, y0, prm: OracleParams, w=None) -> Fit:
         for _ in range(prm.max_backtracks):
             trial = res - alpha * ud
             n_cost += 1
-            if lp_cost(trial, prm.p, prm.mu, w) <= f + prm.sufficient_decrease * alpha * slope:
+            tc = lp_cost(trial, prm.p, prm.mu, w)
+            rhs = f + prm.sufficient_decrease * alpha * slope
+            margin = min(margin, abs(tc - rhs) / max(abs(f), 1e-300))
+            if tc <= rhs:
                 ok = True
                 break
             alpha *= prm.shrink
@@ -175,7 +184,7 @@ def fit(U: np.ndarray, x: np.ndarray, y0, prm: OracleParams, w=None) -> Fit:
         beta = max(0.0, float(gr_new @ (gr_new - gr)) / (gnorm * gnorm))
         d = -gr_new + beta * d
         gr = gr_new
-    return Fit(y, res, f, done_iters, n_cost, n_grad)
+    return Fit(y, res, f, done_iters, n_cost, n_grad, margin)
 
 
 # --------------------------------------------------------------------------

@@ -108,7 +108,7 @@ class SceneStream:
             bg = bg[:, y0:y0 + s.height, x0:x0 + s.width]
         return np.clip(bg, 0.0, 1.0)
 
-    def _paint(self, img: np.ndarray) -> None:
+    def _paint(self, img: np.ndarray, fg=None) -> None:
         s = self.spec
         yy, xx = self._grid
         for ob in self._objects:
@@ -118,9 +118,13 @@ class SceneStream:
                 sel = ((yy - cy) / (h / 2.0)) ** 2 + ((xx - cx) / (w / 2.0)) ** 2 <= 1.0
                 for c in range(s.channels):
                     img[c][sel] = color[c]
+                if fg is not None:
+                    fg[sel] = 1
             else:
                 for c in range(s.channels):
                     img[c, y0:y0 + h, x0:x0 + w] = color[c]
+                if fg is not None:
+                    fg[y0:y0 + h, x0:x0 + w] = 1
             # advance with bouncing
             ny, nx = y0 + vy, x0 + vx
             if ny < 0 or ny + h > s.height:
@@ -131,20 +135,29 @@ class SceneStream:
                 nx = min(max(x0 + vx, 0), s.width - w)
             ob[0], ob[1], ob[4], ob[5] = ny, nx, vy, vx
 
-    def next_frames(self, count: int) -> np.ndarray:
-        """Return the next `count` frames as a (count, n) array (channel-planar)."""
+    def next_frames(self, count: int, truth: bool = False):
+        """Return the next `count` frames as a (count, n) array (channel-planar).
+
+        With `truth=True` also the ground truth the frames were drawn from
+        (same random stream): (frames, foreground masks u8 (count, pixels),
+        clean backgrounds (count, n))."""
         s = self.spec
         out = np.empty((count, s.n), dtype=self.dtype)
+        if truth:
+            fgs = np.zeros((count, s.pixels), dtype=np.uint8)
+            bgs = np.empty((count, s.n))
         for i in range(count):
             img = self._background()
+            if truth:
+                bgs[i] = img.reshape(-1)
             if self._t >= s.fg_from:
-                self._paint(img)
+                self._paint(img, fgs[i].reshape(s.height, s.width) if truth else None)
             if s.noise > 0.0:
                 img = img + self._rng.normal(0.0, s.noise, size=img.shape)
             out[i] = np.clip(img, 0.0, 1.0).reshape(-1)
             self._coef = self._coef + s.walk * self._rng.standard_normal(s.rank)
             self._t += 1
-        return out
+        return (out, fgs, bgs) if truth else out
 
 
 # Tracker settings per BASELINE config (SURVEY.md §8(d)); the generator specs
