@@ -363,7 +363,8 @@ def main():
     elif mode:
         kernel_path = (f"{'tmem' if mode == 2 else 'register'}-resident: "
                        f"{native.query(nat.Q_TEAMS)} teams x "
-                       f"{native.query(nat.Q_TEAM)} CTAs, one cooperative launch per step")
+                       f"{native.query(nat.Q_TEAM)} CTAs x {native.query(nat.Q_GROUPS)} slot groups, "
+                       "one cooperative launch per step")
     else:
         kernel_path = f"streamed: {native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel"
     mask = torch.empty((S, P_loc), dtype=torch.uint8, device=f"cuda:{dev}")

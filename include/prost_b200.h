@@ -159,6 +159,8 @@ int prost_last_error(prost_handle* h, char* buf, int32_t len);
 #define PROST_Q_RESIDENT 5   /* 0 streamed, 1 register-resident, 2 TMEM-resident kernel */
 #define PROST_Q_TEAM 6       /* CTAs per team (resident mode) */
 #define PROST_Q_TEAMS 7      /* teams (resident mode) */
+#define PROST_Q_GROUPS 8     /* slot groups per CTA of the TMEM kernel: streams per team in flight */
+#define PROST_Q_QPC 9        /* row groups (4 coordinates) per CTA slice (resident modes) */
 int prost_query(prost_handle* h, int32_t what, int64_t* value);
 
 /* Per-phase device timing (CUDA events around every launch, on the launch

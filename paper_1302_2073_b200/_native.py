@@ -21,7 +21,7 @@ ERR_CONFIG, ERR_DIMENSION, ERR_NONFINITE, ERR_SEQUENCE, ERR_CUDA = 1, 2, 3, 4, 5
 F32, F64, U8 = 0, 1, 2
 FLAG_PIPELINE, FLAG_FP64, FLAG_LATENCY = 1, 2, 4
 Q_LAUNCHES, Q_WAVE, Q_BYTES_U, Q_CHUNKS, Q_INSTANCE_K = 0, 1, 2, 3, 4
-Q_RESIDENT, Q_TEAM, Q_TEAMS = 5, 6, 7
+Q_RESIDENT, Q_TEAM, Q_TEAMS, Q_GROUPS, Q_QPC = 5, 6, 7, 8, 9
 
 EXPORTS = (
     "prost_abi_version", "prost_create", "prost_destroy", "prost_set_core_state",

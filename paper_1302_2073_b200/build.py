@@ -12,14 +12,15 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = PKG / "csrc" / "prost_b200.cu"
+# translation units, compiled in parallel and linked into one library
+SRCS = [PKG / "csrc" / n for n in ("prost_b200.cu", "tmem_k.cu", "resident_k.cu")]
 DEPS = sorted((PKG / "csrc").glob("*.cu*")) + sorted((ROOT / "include").glob("*.h")) + [
     Path(__file__).resolve()]
 OUT = PKG / "_lib" / "libprost_b200.so"
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-shared", f"-I{ROOT / 'include'}",
+    "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}",
     # fp32 denormals flushed: every penalty input is >= mu > 0, and rsqrtf then
     # maps to a single MUFU.RSQ (the fp64 parity instantiation is unaffected)
     "-ftz=true",
@@ -40,18 +41,36 @@ def up_to_date() -> bool:
     return all(d.stat().st_mtime <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: Path = OUT, extra=()) -> Path:
+    """Compile every translation unit (in parallel) and link the shared
+    library; `extra` adds nvcc flags (experiment variants, e.g. -DPROST_WC=3)."""
+    if not force and out == OUT and not extra and up_to_date():
         return OUT
-    OUT.parent.mkdir(parents=True, exist_ok=True)
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), str(SRC)]
+    out.parent.mkdir(parents=True, exist_ok=True)
+    objdir = PKG / "_lib" / "obj" / out.stem
+    objdir.mkdir(parents=True, exist_ok=True)
+    procs = []
+    for src in SRCS:
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", str(obj), str(src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append((subprocess.Popen(cmd), obj))
+    failed = [obj for p, obj in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc ({', '.join(o.name for o in failed)})")
+    tmp = out.with_suffix(".so.tmp")
+    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp),
+            *[str(obj) for _, obj in procs]]
     if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+        print(" ".join(link), flush=True)
+    subprocess.run(link, check=True)
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    out = Path(args[0]) if args and not args[0].startswith("-") else OUT
+    extra = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose=True, out=out, extra=extra))

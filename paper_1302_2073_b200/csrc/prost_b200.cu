@@ -21,8 +21,10 @@
 #include "prost_phases.cuh"
 #include "prost_resident.cuh"
 #include "prost_tmem.cuh"
+#include "kernel_ops.h"
 
 using namespace prost;
+using namespace prost_ops;
 
 static_assert(sizeof(FitInfo) == sizeof(prost_fit_info), "FitInfo layout");
 
@@ -55,6 +57,7 @@ struct prost_handle {
   bool resident = false;
   bool tmem = false;
   int rG = 0, rT = 0, rqpc = 0, rnt = 0;
+  int rng = 1;  // k_tmem slot groups per CTA
   size_t rsmem = 0;
   unsigned* rbar = nullptr;
   double* rpart = nullptr;
@@ -74,12 +77,20 @@ struct prost_handle {
   double* rinv = nullptr;
   FitInfo* info = nullptr;
   FitInfo* info_h = nullptr;  // pinned
+  // non-blocking look at the FitInfo of the last push without a readback
+  // (fit == nullptr): decides when the cold-start kernel can be skipped
+  FitInfo* info_peek = nullptr;  // pinned
+  cudaEvent_t ev_peek = nullptr;
+  bool peek_pending = false;
   // lazily allocated
   void* bgbuf = nullptr;
   void* resbuf = nullptr;
   uint8_t* maskbuf = nullptr;
-  void* stage = nullptr;
-  size_t stage_bytes = 0;
+  // conversion staging: uploads (frames) and downloads (outputs) have their
+  // own buffers, so a pipelined push's upload of frame N+1 on s_in never
+  // overwrites frame N's outputs still being converted / copied out on s_out
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes[2] = {0, 0};
   long long launches = 0;
   bool maybe_cold = true;
   // upper bound on every stream's steps-since-QR before the next push: the
@@ -317,110 +328,6 @@ struct Impl {
   }
 };
 
-// Register-resident frame kernel (prost_resident.cuh), fp32, one channel.
-struct ResOps {
-  cudaError_t (*launch)(const Args&, const RArgs&, int nt, size_t smem, cudaStream_t st);
-  cudaError_t (*prepare)(size_t smem);
-  int (*occupancy)(int nt, size_t smem);
-  size_t (*smem)(int qpc, int nwarp);
-  int ntmax;
-};
-
-template <int K, int NTMAX, int PM>
-struct Res {
-  static cudaError_t launch(const Args& a, const RArgs& ra, int nt, size_t smem, cudaStream_t st) {
-    Args aa = a;
-    RArgs rr = ra;
-    void* args[] = {&aa, &rr};
-    return cudaLaunchCooperativeKernel((const void*)k_resident<K, NTMAX, PM>, dim3(ra.T * ra.G),
-                                       dim3(nt), args, smem, st);
-  }
-  static cudaError_t prepare(size_t smem) {
-    return cudaFuncSetAttribute(k_resident<K, NTMAX, PM>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  static int occupancy(int nt, size_t smem) {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_resident<K, NTMAX, PM>, nt, smem) !=
-        cudaSuccess)
-      return 0;
-    return nb;
-  }
-  static size_t smem(int qpc, int nwarp) { return resident_smem<K>(qpc, nwarp); }
-  static ResOps ops() { return ResOps{&launch, &prepare, &occupancy, &smem, NTMAX}; }
-};
-
-// p = 0.5 (every BASELINE config) gets its own instance with the two-RSQ
-// penalty; other exponents use the runtime-dispatched instance.
-// 512 threads x 128 registers for k <= 16: the 60 basis registers of a 4-row
-// group plus the CG working set (ptxas budgets registers per 128-thread granule).
-ResOps pick_resident(int K, bool half) {
-  switch (K) {
-    case 4: return half ? Res<4, 768, PM_HALF>::ops() : Res<4, 768, PM_ANY>::ops();
-    case 8: return half ? Res<8, 768, PM_HALF>::ops() : Res<8, 768, PM_ANY>::ops();
-    case 15: return half ? Res<15, 512, PM_HALF>::ops() : Res<15, 512, PM_ANY>::ops();
-    case 16: return half ? Res<16, 512, PM_HALF>::ops() : Res<16, 512, PM_ANY>::ops();
-    default: return ResOps{nullptr, nullptr, nullptr, nullptr, 0};
-  }
-}
-
-// TMEM-resident frame kernel (prost_tmem.cuh), fp32, one channel, k <= 16.
-struct TmOps {
-  cudaError_t (*launch)(const Args&, const RArgs&, size_t smem, cudaStream_t st);
-  cudaError_t (*prepare)(size_t smem);
-  int (*occupancy)(size_t smem);
-  size_t (*smem)(int qpc);
-  int qt;  // row groups per thread held in TMEM
-  void (*describe)();
-};
-
-template <int K, int PM>
-struct Tm {
-  static cudaError_t launch(const Args& a, const RArgs& ra, size_t smem, cudaStream_t st) {
-    Args aa = a;
-    RArgs rr = ra;
-    void* args[] = {&aa, &rr};
-    if (TM_CPS == 1)
-      return cudaLaunchCooperativeKernel((const void*)k_tmem<K, PM>, dim3(ra.T * ra.G), dim3(TM_NT),
-                                         args, smem, st);
-    // The occupancy calculator reports one CTA per SM for any kernel that
-    // allocates tensor memory, so a cooperative launch of TM_CPS CTAs per SM is
-    // refused; the hardware co-schedules them (tools/probe/coresid_probe.cu),
-    // and the grid is sized to the chip, so every CTA is resident at once.
-    return cudaLaunchKernel((const void*)k_tmem<K, PM>, dim3(ra.T * ra.G), dim3(TM_NT), args, smem, st);
-  }
-  static cudaError_t prepare(size_t smem) {
-    return cudaFuncSetAttribute(k_tmem<K, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  static int occupancy(size_t smem) {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tmem<K, PM>, TM_NT, smem) != cudaSuccess)
-      return 0;
-    return nb;
-  }
-  static size_t smem(int qpc) { return tmem_smem<K>(qpc); }
-  static void describe() {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_tmem<K, PM>);
-    int nb0 = -1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, k_tmem<K, PM>, TM_NT, 0);
-    fprintf(stderr, "prost: k_tmem<%d> regs %d local %zu static smem %zu max threads %d; occupancy(smem 0) %d\n",
-            K, fa.numRegs, fa.localSizeBytes, fa.sharedSizeBytes, fa.maxThreadsPerBlock, nb0);
-  }
-  static TmOps ops() { return TmOps{&launch, &prepare, &occupancy, &smem, TmemGeom<K>::QT, &describe}; }
-};
-
-TmOps pick_tmem(int K, bool half) {
-  switch (K) {
-    case 4: return half ? Tm<4, PM_HALF>::ops() : Tm<4, PM_ANY>::ops();
-    case 8: return half ? Tm<8, PM_HALF>::ops() : Tm<8, PM_ANY>::ops();
-    case 15: return half ? Tm<15, PM_HALF>::ops() : Tm<15, PM_ANY>::ops();
-    case 16: return half ? Tm<16, PM_HALF>::ops() : Tm<16, PM_ANY>::ops();
-    case 20: return half ? Tm<20, PM_HALF>::ops() : Tm<20, PM_ANY>::ops();
-    default: return TmOps{nullptr, nullptr, nullptr, nullptr, 0, nullptr};
-  }
-}
-
 template <typename T>
 Ops pick(int k) {
 #define PROST_K(KK) \
@@ -477,13 +384,14 @@ void* dev_alloc(size_t bytes, cudaError_t* e) {
   return p;
 }
 
-int ensure_stage(prost_handle* h, size_t bytes) {
-  if (h->stage_bytes >= bytes) return PROST_OK;
-  if (h->stage) cudaFree(h->stage);
-  h->stage = nullptr;
-  h->stage_bytes = 0;
-  CK(cudaMalloc(&h->stage, bytes));
-  h->stage_bytes = bytes;
+enum { STAGE_IN = 0, STAGE_OUT = 1 };
+int ensure_stage(prost_handle* h, int which, size_t bytes) {
+  if (h->stage_bytes[which] >= bytes) return PROST_OK;
+  if (h->stage[which]) cudaFree(h->stage[which]);
+  h->stage[which] = nullptr;
+  h->stage_bytes[which] = 0;
+  CK(cudaMalloc(&h->stage[which], bytes));
+  h->stage_bytes[which] = bytes;
   return PROST_OK;
 }
 
@@ -503,10 +411,10 @@ int upload_dense(prost_handle* h, const void* src, int dt, int on_device, void* 
   }
   const void* dsrc = src;
   if (!on_device) {
-    int rc = ensure_stage(h, (size_t)rows * P * dsz);
+    int rc = ensure_stage(h, STAGE_IN, (size_t)rows * P * dsz);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(h->stage, src, (size_t)rows * P * dsz, cudaMemcpyHostToDevice, st));
-    dsrc = h->stage;
+    CK(cudaMemcpyAsync(h->stage[STAGE_IN], src, (size_t)rows * P * dsz, cudaMemcpyHostToDevice, st));
+    dsrc = h->stage[STAGE_IN];
   }
   const int nb = blocks_for((long long)rows * P);
   const double sc = dt == PROST_U8 ? 1.0 / 255.0 : 1.0;
@@ -537,9 +445,9 @@ int download_dense(prost_handle* h, const void* src, void* dst, int dt, int on_d
   if (dt == PROST_U8) return fail(h, PROST_ERR_CONFIG, "u8 is an input-only dtype");
   void* ddst = dst;
   if (!on_device) {
-    int rc = ensure_stage(h, (size_t)rows * P * dsz);
+    int rc = ensure_stage(h, STAGE_OUT, (size_t)rows * P * dsz);
     if (rc) return rc;
-    ddst = h->stage;
+    ddst = h->stage[STAGE_OUT];
   }
   const int nb = blocks_for((long long)rows * P);
   if (h->fp64) k_pack<double, float><<<nb, NT, 0, st>>>((const double*)src, (float*)ddst, rows, 1, P, Pp, 0, 1.0);
@@ -554,6 +462,15 @@ int copy_labels(prost_handle* h, const uint8_t* src, uint8_t* dst, int on_device
   CK(cudaMemcpy2DAsync(dst, h->P, src, h->Pp, h->P, h->S,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   return PROST_OK;
+}
+
+// Retire a finished non-blocking FitInfo peek (see push_outputs).
+void retire_peek(prost_handle* h) {
+  if (!h->peek_pending || cudaEventQuery(h->ev_peek) != cudaSuccess) return;
+  bool cold = false;
+  for (int s = 0; s < h->S; ++s) cold |= h->info_peek[s].frame_index == 0;
+  h->maybe_cold = cold;
+  h->peek_pending = false;
 }
 
 int check_stream(prost_handle* h, int s) {
@@ -586,6 +503,7 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   if (dtype != PROST_F32 && dtype != PROST_F64 && dtype != PROST_U8)
     return fail(h, PROST_ERR_CONFIG, "unknown frame dtype %d", dtype);
   CK(cudaSetDevice(h->device));
+  retire_peek(h);
   // A QR is due in this push only for a stream whose steps-since-QR is already
   // QR_EVERY - 1 (manifold.py:192).  Near that bound, refresh it from the
   // device (one small synchronous read every ~QR_EVERY frames).
@@ -651,7 +569,6 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
 int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStream_t st) {
   const int odt = o.dtype == PROST_F64 ? PROST_F64 : PROST_F32;
   CK(cudaGetLastError());
-  h->maybe_cold = false;
   // outputs the kernels could not write in place
   int rc = PROST_OK;
   if (o.background && a.bg_out == h->bgbuf)
@@ -666,11 +583,21 @@ int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStr
     CK(cudaStreamSynchronize(st));
     std::memcpy(o.fit, h->info_h, (size_t)h->S * sizeof(FitInfo));
     int first_bad = PROST_OK;
+    bool cold = false;
     for (int s = 0; s < h->S; ++s) {
       if (h->info_h[s].status != PROST_OK && first_bad == PROST_OK) first_bad = h->info_h[s].status;
-      if (h->info_h[s].status != PROST_OK && h->info_h[s].frame_index == 0) h->maybe_cold = true;
+      cold |= h->info_h[s].frame_index == 0;  // rejected at its first frame: still cold
     }
+    h->maybe_cold = cold;
+    h->peek_pending = false;
     if (first_bad != PROST_OK) return fail(h, first_bad, "frame contains non-finite values");
+  } else if (h->maybe_cold && !h->peek_pending) {
+    // no readback requested: peek at the frame indices asynchronously and
+    // keep launching the cold-start kernel until every stream is past frame 0
+    // (a stream whose first frame was rejected stays cold, fit.py:86-87)
+    CK(cudaMemcpyAsync(h->info_peek, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(h->ev_peek, st));
+    h->peek_pending = true;
   }
   return PROST_OK;
 }
@@ -681,14 +608,16 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
     // one cooperative launch for the whole frame of every stream, then the median
     const char* stg = getenv("PROST_STAGGER_NS");
     const char* pfe = getenv("PROST_PREFETCH");  // 1: k_tmem L2 prefetch of the next stream (measured slower)
+    const char* alt = getenv("PROST_ALT");       // 0: slot groups load independently
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
-             h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0};
-    CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * sizeof(unsigned), st));
+             h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0,
+             alt ? atoi(alt) : 1};
+    CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
     long long n = 0;
     {
       PhaseTimer pt_(h, st, PROST_PH_FRAME);
       if (h->tmem)
-        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rsmem, st));
+        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng).launch(a, ra, h->rsmem, st));
       else
         CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
       ++n;
@@ -855,6 +784,8 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   ALLOC(rinv, S * KMAX * KMAX * sizeof(double));
   ALLOC(info, S * sizeof(FitInfo));
   CK(cudaMallocHost(&h->info_h, S * sizeof(FitInfo)));
+  CK(cudaMallocHost(&h->info_peek, S * sizeof(FitInfo)));
+  CK(cudaEventCreateWithFlags(&h->ev_peek, cudaEventDisableTiming));
   // Resident frame kernel: fp32, one channel, k <= 16, and a team that fits the
   // chip.  The geometry depends on the stream shape only (not on n_streams), so
   // a stream's reduction order — and its result — is the same in any batch.
@@ -866,18 +797,28 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   std::string kpath = kenv ? kenv : (want_res && want_res[0] == '1' ? "resident" : "tmem");
   if (no_res && no_res[0] == '1') kpath = "streamed";
   const bool eligible = !h->fp64 && K <= 20;
-  const TmOps to = pick_tmem(K, params->p == 0.5);
+  // slot groups per CTA (prost_tmem.cuh): 1; PROST_TM_GROUPS=2 (two streams
+  // per CTA in parallel warp groups) is kept as an experiment switch and
+  // falls back to 1 when that instance is not built (measured slower)
+  const char* ngenv = getenv("PROST_TM_GROUPS");
+  int ng = ngenv ? atoi(ngenv) : 1;
+  if (ng != 1 && ng != 2) ng = 1;
+  const char* genv = getenv("PROST_TM_G");  // force the team size (experiments)
+  const int force_G = genv ? atoi(genv) : 0;
+  for (int attempt = 0; attempt < 2 && !h->tmem; ++attempt, ng = 1) {
+  const TmOps to = pick_tmem(K, params->p == 0.5, ng);
   if (eligible && kpath == "tmem" && to.launch) {
     if (getenv("PROST_DEBUG")) to.describe();
     // Team size: among the slices that fit TMEM + shared memory, the one with
     // the most stream frames per unit time, teams / round time, with the round
     // time modelled as a fixed part (reduction latency, ~1.5 slot sweeps as
     // measured on C3) plus one part per row-group slot a thread walks (every
-    // thread of a CTA walks the same number of slots, so a slice just over a
+    // thread of a group walks the same number of slots, so a slice just over a
     // slot boundary costs a whole extra slot).  Depends on the stream shape
     // and the chip only (not on n_streams): per-stream results do not depend
     // on the batch.
     const int nq = (int)(h->np / 4);  // row groups over all channel planes
+    const int tg = TM_NT / ng;         // threads per slot group
     int bestG = 0;
     double best_cost = 0;
     for (int G = 1; G <= sms; ++G) {
@@ -885,11 +826,13 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
       if ((nq + qpc - 1) / qpc != G) continue;
       const size_t sm = to.smem(qpc);
       if (sm > (size_t)227 * 1024) continue;
-      const int slots = (qpc + TM_NT - 1) / TM_NT;
-      // throughput: teams / round time; latency (PROST_FLAG_LATENCY): the round
-      // time of one stream, slots per thread plus a small per-CTA barrier cost
+      if (force_G > 0 && G != force_G) continue;
+      const int slots = (qpc + tg - 1) / tg;
+      // throughput: virtual teams / round time; latency (PROST_FLAG_LATENCY):
+      // the round time of one stream, slots per thread plus a small per-CTA
+      // barrier cost
       const double cost = (flags & PROST_FLAG_LATENCY) ? slots + 0.05 * G
-                                                       : (1.5 + slots) / (double)(sms * TM_CPS / G);
+                                                       : (1.5 + slots) / (double)(sms * TM_CPS / G * ng);
       if (bestG == 0 || cost < best_cost) {
         bestG = G;
         best_cost = cost;
@@ -912,20 +855,25 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
       }
       {
         h->tmem = true;
+        h->rng = ng;
         h->rqpc = qpc;
         h->rnt = TM_NT;
         h->rsmem = sm;
         h->rG = G;
-        h->rT = std::min(h->S, sms * TM_CPS / G);
+        // enough teams for every stream to have a slot group, at most the chip
+        h->rT = std::min((h->S + ng - 1) / ng, sms * TM_CPS / G);
         h->resident_ops_K = K;
         if (h->C == 3) ALLOC(labc, S * np);
-        ALLOC(rbar, (size_t)sms * TM_CPS * sizeof(unsigned));
-        ALLOC(rpart, (size_t)2 * sms * TM_CPS * RES_RNV_MAX * sizeof(double));
+        ALLOC(rbar, (size_t)sms * TM_CPS * 2 * sizeof(unsigned));
+        ALLOC(rpart, (size_t)2 * sms * TM_CPS * 2 * RES_RNV_MAX * sizeof(double));
         ALLOC(rprof, (size_t)sms * TM_CPS * PROF_N * sizeof(unsigned long long));
+        if (getenv("PROST_DEBUG"))
+          fprintf(stderr, "prost: tmem NG=%d G=%d T=%d qpc=%d smem=%zu\n", ng, G, h->rT, qpc, sm);
       }
       cudaGetLastError();
       break;
     }
+  }
   }
   const ResOps ro = pick_resident(K, params->p == 0.5);
   if (eligible && h->C == 1 && ro.launch && kpath == "resident") {
@@ -986,7 +934,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
 void prost_destroy(prost_handle* h) {
   if (!h) return;
   void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
-                  h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage,
+                  h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage[0], h->stage[1],
                   h->rbar, h->rpart, h->rprof, h->xred, h->xgo, h->labc};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1010,6 +958,8 @@ void prost_destroy(prost_handle* h) {
     }
   }
   if (h->info_h) cudaFreeHost(h->info_h);
+  if (h->info_peek) cudaFreeHost(h->info_peek);
+  if (h->ev_peek) cudaEventDestroy(h->ev_peek);
   for (auto& pe : h->prof_ev) {
     cudaEventDestroy(pe.second.first);
     cudaEventDestroy(pe.second.second);
@@ -1065,7 +1015,10 @@ int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const
   c.status = ST_OK;
   c.active = 0;
   CK(cudaMemcpy(h->ctl + stream, &c, sizeof c, cudaMemcpyHostToDevice));
-  if (frame_index == 0) h->maybe_cold = true;
+  if (frame_index == 0) {
+    h->maybe_cold = true;
+    h->peek_pending = false;  // an older peek predates this state
+  }
   return PROST_OK;
 }
 
@@ -1447,6 +1400,8 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value) {
     case PROST_Q_RESIDENT: *value = h->tmem ? 2 : (h->resident ? 1 : 0); break;
     case PROST_Q_TEAM: *value = h->rG; break;
     case PROST_Q_TEAMS: *value = h->rT; break;
+    case PROST_Q_GROUPS: *value = h->rng; break;
+    case PROST_Q_QPC: *value = h->rqpc; break;
     default: return fail(h, PROST_ERR_CONFIG, "unknown query %d", what);
   }
   return PROST_OK;
@@ -1493,7 +1448,7 @@ int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n) {
   // converted from SM clocks to ns with the CTA's own clock rate), then the
   // max kernel time
   const bool is_time[PROF_N] = {true, true, true, true, true, false, false,
-                                true, true, true, true, false};
+                                true, true, true, true, false, true, true};
   std::vector<double> acc(PROF_N, 0.0);
   unsigned long long mx = 0;
   for (int c = 0; c < ctas; ++c) {

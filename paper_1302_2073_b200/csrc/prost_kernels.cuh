@@ -68,7 +68,7 @@ struct Ctl {
   double pend_alpha;   // residual update r -= pend_alpha * u_dir not yet applied
   double acc_alpha, acc_cost;
   double std_cur;      // normalization scale of this frame
-  double t, geo_a, geo_s, geo_ln;
+  double t, geo_a, geo_s, geo_ln, geo_yn;  // geo_yn = ||y|| (the relabel's U'y update)
   double psum, psumsq, pstd;
   long long pcount, pseen, frame_index, since_qr;
   int it, active, need_lsfb, need_gradfb, acc_idx, ls_next, gwin_lo, last_acc;
@@ -389,6 +389,7 @@ __device__ PROST_LOGIC void finish_frame(Ctl* c, const Args& a, int s, int lane)
       c->geo_a = cphi - 1.0;
       c->geo_s = sphi;
       c->geo_ln = ln;
+      c->geo_yn = rn;
       c->since_qr += 1;
       c->qr_now = c->since_qr >= QR_EVERY ? 1 : 0;
     }

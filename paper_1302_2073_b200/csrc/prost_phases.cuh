@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
 // ---------------------------------------------------------------------------
 // k_median: 3x3 majority vote with edge replication (pipeline.py:215-228).
 
-__global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
+static __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
 // three rows are one 32-bit add (labels are 0/1, sums <= 3 per byte); the
 // horizontal window adds the word shifted by one byte each way, with the
 // neighbouring columns (edge-replicated) shifted in; >= 5 is __vcmpgeu4.
-__global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) {
+static __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   const int W = a.width, H = a.height, wq = W >> 2;
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) 
 
 // k_median16: sixteen pixels per thread (widths that are a multiple of 16):
 // three 16-byte row loads and two edge bytes per row per 16 pixels.
-__global__ void __launch_bounds__(NT) k_median16(const __grid_constant__ Args a) {
+static __global__ void __launch_bounds__(NT) k_median16(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   const int W = a.width, H = a.height, wq = W >> 4;
@@ -905,7 +905,7 @@ __global__ void k_resample(const TI* __restrict__ src, TO* __restrict__ dst, int
   }
 }
 
-__global__ void k_upsample_mask(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int w_in,
+static __global__ void k_upsample_mask(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int w_in,
                                 int h_in, int w_out, int h_out) {
   const long long total = (long long)w_out * h_out;
   const double fx = (double)w_in / (double)w_out, fy = (double)h_in / (double)h_out;
@@ -924,7 +924,7 @@ __global__ void k_upsample_mask(const uint8_t* __restrict__ src, uint8_t* __rest
 // unknown (170) are not scored, 255 is foreground, every other value
 // background.  Integer atomics: exact and order-independent.
 
-__global__ void __launch_bounds__(NT) k_confusion(const uint8_t* __restrict__ mask,
+static __global__ void __launch_bounds__(NT) k_confusion(const uint8_t* __restrict__ mask,
                                                   const uint8_t* __restrict__ truth, int P,
                                                   long long mask_stride, unsigned long long* counts) {
   const int s = blockIdx.y;
@@ -971,7 +971,7 @@ __global__ void k_unpack_pnm(const uint8_t* __restrict__ payload, int C, int P, 
 // 210-211) from the TMEM kernel's per-coordinate flags; streams whose frame
 // was rejected keep their labels.
 
-__global__ void __launch_bounds__(NT) k_combine3(const __grid_constant__ Args a) {
+static __global__ void __launch_bounds__(NT) k_combine3(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   const uint32_t* F = reinterpret_cast<const uint32_t*>(a.labc + (size_t)s * a.np);

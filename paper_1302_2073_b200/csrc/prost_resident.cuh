@@ -33,6 +33,7 @@ struct RArgs {
   unsigned long long* prof;  // [gridDim][8] optional timing counters (ns), or null
   int stagger_ns;            // start delay of odd teams (k_tmem), 0 = none
   int prefetch;              // k_tmem: L2 prefetch of the next stream's slice
+  int alt;                   // k_tmem with 2 slot groups: alternate the groups' slice loads
 };
 
 // Timing counters of one CTA (thread 0, %globaltimer ns): see PROF_* below.
@@ -40,6 +41,8 @@ enum {
   PROF_TOTAL = 0, PROF_BARRIER, PROF_SLOTS, PROF_LOGIC, PROF_PREFETCH, PROF_NSUMS, PROF_ROUNDS,
   PROF_T_STATS, PROF_T_PASS0, PROF_T_ITER, PROF_T_GEO,  // phase wall times (k_tmem)
   PROF_GT_TOTAL,  // kernel time in %globaltimer ns (the others count SM clocks)
+  PROF_SW_OWN,    // k_tmem CG iteration sweeps: thread 0's own sweep + staging
+  PROF_SW_ALL,    //   ... until every warp of the CTA has staged its partials
   PROF_N = 16
 };
 

@@ -26,6 +26,29 @@
 
 #include <type_traits>
 
+#include "prost_logic_fast.cuh"
+#ifndef PROST_FAST_LOGIC
+#define PROST_FAST_LOGIC 1
+#endif
+#if PROST_FAST_LOGIC
+#if PROST_OLD_PASS0
+#define TM_AFTER_PASS0 after_pass0
+#else
+#define TM_AFTER_PASS0 fl_after_pass0
+#endif
+#if PROST_OLD_ITER
+#define TM_AFTER_ITER after_iter
+#else
+#define TM_AFTER_ITER fl_after_iter
+#endif
+#define TM_AFTER_LSFB fl_after_lsfb
+#define TM_AFTER_GRADFB fl_after_gradfb
+#else
+#define TM_AFTER_PASS0 after_pass0
+#define TM_AFTER_ITER after_iter
+#define TM_AFTER_LSFB after_lsfb
+#define TM_AFTER_GRADFB after_gradfb
+#endif
 #include "prost_resident.cuh"
 #include "tmem_io.cuh"
 
@@ -61,16 +84,115 @@ struct TmemGeom {
   static constexpr int NV = NV0 > NV1 ? NV0 : NV1;
 };
 
-// Dynamic shared memory of k_tmem<K> for qpc row groups per CTA.
-template <int K>
-__host__ __device__ constexpr size_t tmem_smem(int qpc) {
+// Dynamic shared memory of one slot group of k_tmem<K, PM, NG> (TM_NT / NG
+// threads) for qpc row groups per CTA slice.
+template <int K, int NG>
+__host__ __device__ constexpr size_t tmem_group_smem(int qpc) {
   using Geo = TmemGeom<K>;
-  const int qs = qpc > Geo::QT * TM_NT ? qpc - Geo::QT * TM_NT : 0;
-  const int qa = (qpc + TM_NT - 1) / TM_NT * TM_NT;  // r / u_dir arrays cover whole slots
-  return (size_t)16 * Geo::RS * qs                     // basis row groups kept in shared memory
-         + (size_t)qa * 32                             // r, u_dir
-         + (Geo::WCOL ? 0 : (size_t)qa * 4)            // label words
-         + (size_t)(TM_NT / 32 + 1) * Geo::NV * 8 + sizeof(Ctl) + 64;
+  constexpr int TG = TM_NT / NG;
+  const int qs = qpc > Geo::QT * TG ? qpc - Geo::QT * TG : 0;
+  const int qa = (qpc + TG - 1) / TG * TG;  // r / u_dir arrays cover whole slots
+  return ((size_t)16 * Geo::RS * qs        // basis row groups kept in shared memory
+          + (size_t)qa * 32                // r, u_dir
+          + (Geo::WCOL ? 0 : (size_t)qa * 4)  // label words
+          + (size_t)(TG / 32 + 1) * Geo::NV * 8 + sizeof(Ctl) + 127) / 128 * 128;
+}
+template <int K, int NG = 1>
+__host__ __device__ constexpr size_t tmem_smem(int qpc) {
+  return NG * tmem_group_smem<K, NG>(qpc) + 64;
+}
+
+// Named barrier of one slot group (ids 1.., TG threads); NG == 1 uses the CTA barrier.
+template <int NG>
+__device__ __forceinline__ void group_sync(int g) {
+  if constexpr (NG == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(TM_NT / NG) : "memory");
+  }
+}
+
+// team_sum / rstage / stage_floats of one slot group: wred is the group's
+// [TG/32][nv] staging, lt the thread within the group; the team's slots and
+// barrier counter are those of virtual team vt.
+template <int NG>
+__device__ __forceinline__ void team_sum_g(const RArgs& ra, int vt, int VT, int rank, int g, int lt,
+                                           const double* wred, int nv, double* red, unsigned& epoch,
+                                           unsigned long long* sprof) {
+  constexpr int TG = TM_NT / NG, NWG = TG / 32;
+  group_sync<NG>(g);
+  const bool tp = ra.prof && g == 0 && lt == 0;
+  unsigned long long t0 = tp ? ptimer() : 0;
+  const int warp = lt >> 5, lane = lt & 31;
+  const int G = ra.G;
+  const int par = epoch & 1;
+  double* area = ra.rpart + ((size_t)par * VT + vt) * (size_t)ra.rnv * G;
+  for (int v = lt; v < nv; v += TG) {
+    double acc = 0.0;
+    for (int w = 0; w < NWG; ++w) acc += wred[w * nv + v];
+    area[(size_t)v * G + rank] = acc;
+  }
+  ++epoch;
+  group_sync<NG>(g);
+  if (lt == 0) {
+    unsigned* ctr = ra.bar + vt;
+    const unsigned target = epoch * (unsigned)G;
+    red_release_add(ctr, 1u);
+    long long spins = 0;
+    while (ld_acquire(ctr) < target) {
+      if (++spins > (1LL << 26)) __trap();
+    }
+  }
+  group_sync<NG>(g);
+  unsigned long long t1 = tp ? ptimer() : 0;
+  for (int v0 = warp; v0 < nv; v0 += 4 * NWG) {
+    double acc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[i] = 0.0;
+      const int v = v0 + i * NWG;
+      if (v < nv) {
+        const double* b = area + (size_t)v * G;
+#pragma unroll
+        for (int c = 0; c < 5; ++c)  // G <= 160: up to 5 independent loads per lane
+          if (lane + 32 * c < G) acc[i] += __ldcg(b + lane + 32 * c);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double t = warp_sum(acc[i]);
+      const int v = v0 + i * NWG;
+      if (lane == 0 && v < nv) red[v] = t;
+    }
+  }
+  group_sync<NG>(g);
+  if (tp) {
+    const unsigned long long t2 = ptimer();
+    sprof[PROF_BARRIER] += t1 - t0;
+    sprof[PROF_SLOTS] += t2 - t1;
+    sprof[PROF_NSUMS] += 1;
+  }
+}
+
+// One double per lane -> its warp sum in wred[lwarp][slot].
+__device__ __forceinline__ void rstage_g(double x, double* wred, int slot, int nv, int lt) {
+  x = warp_sum(x);
+  if ((lt & 31) == 0) wred[(lt >> 5) * nv + slot] = x;
+}
+
+// N floats per lane -> warp sums in wred[lwarp][base .. base+N).
+template <int N>
+__device__ __forceinline__ void stage_floats_g(const float (&v)[N], double* wred, int nv, int base,
+                                               int lt) {
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float t[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t[i] = (c0 + i < N) ? v[c0 + i] : 0.f;
+    const float r = warp_reduce_scatter32(t);
+    const int lane = lt & 31;
+    if (c0 + lane < N) wred[(lt >> 5) * nv + base + c0 + lane] = (double)r;
+  }
 }
 
 template <int RS>
@@ -137,19 +259,33 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <int K, int PM>
+// NG slot groups per CTA (1 or 2): group g (TG = TM_NT / NG threads, TMEM
+// columns [512 g / NG, 512 (g + 1) / NG), its own share of shared memory)
+// works on its own stream: CTA team t's group g is virtual team t * NG + g.
+// With NG = 2 the two groups of an SM are in different phases of their
+// frames, so one group's HBM traffic (slice load, U' store) and its team-sum
+// latency overlap the other group's sweeps (optionally enforced: ra.alt makes
+// the groups' slice loads alternate A, B, A, B, ...).
+template <int K, int PM, int NG>
 __global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
   constexpr int RS = Geo::RS, QW = Geo::QW, QT = Geo::QT, NVM = Geo::NV;
   constexpr bool WCOL = Geo::WCOL;
+  constexpr int TG = TM_NT / NG;  // threads per slot group
+  static_assert(NG == 1 || NG == 2, "slot groups");
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ unsigned s_tbase;
   __shared__ unsigned long long sprof[PROF_N];
-  __shared__ float sfv[4][K];  // fp32 copies of y, d, v, grad for the per-element math
+  __shared__ float sfv_all[NG][4][K];  // fp32 copies of y, d, v, grad for the per-element math
+  __shared__ volatile int s_loads[2], s_done[2];  // slice loads done per group (ra.alt)
   const int G = ra.G, T = ra.T, qpc = ra.qpc;
   const int team = blockIdx.x / G, rank = blockIdx.x - team * G;
   const int tid = threadIdx.x, warp = tid >> 5;
+  const int g = NG == 1 ? 0 : tid / TG;
+  const int lt = tid - g * TG;  // thread within the slot group
+  const int VT = T * NG, vt = team * NG + g;
+  float (&sfv)[4][K] = sfv_all[g];
   const int k = a.k;
   // row groups over the stream's stacked coordinates: with 3 channels a slice
   // may cover parts of several planes (Pp is a multiple of 4: a row group never
@@ -157,24 +293,28 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   const int nq = (int)(a.np / 4);
   const int q0 = rank * qpc;
   const int qcount = max(0, min(qpc, nq - q0));
-  const int nslots = (qcount + TM_NT - 1) / TM_NT;  // uniform across the CTA
-  const int nst = nslots < QT ? nslots : QT;        // TMEM slots in use
-  const int qs = qpc > QT * TM_NT ? qpc - QT * TM_NT : 0;
-  const int qa = (qpc + TM_NT - 1) / TM_NT * TM_NT;
+  const int nslots = (qcount + TG - 1) / TG;  // uniform across the group
+  const int nst = nslots < QT ? nslots : QT;  // TMEM slots in use
+  const int qs = qpc > QT * TG ? qpc - QT * TG : 0;
+  const int qa = (qpc + TG - 1) / TG * TG;
 
   // basis rows kept in shared memory: [row e][4-column group][row group] float4,
   // so a thread reads one row with RS/4 conflict-free 16-byte loads
-  float4* sU = reinterpret_cast<float4*>(smem_raw);     // [4][RS/4][qs]
+  float4* sU = reinterpret_cast<float4*>(smem_raw + (size_t)g * tmem_group_smem<K, NG>(qpc));  // [4][RS/4][qs]
   float4* sR = sU + (size_t)RS * qs;                    // [qa] residual
   float4* sD = sR + qa;                                 // [qa] u_dir
   uint32_t* sL = reinterpret_cast<uint32_t*>(sD + qa);  // [qa] label bytes (!WCOL)
   double* wred = reinterpret_cast<double*>(sL + (WCOL ? 0 : qa));
-  double* red = wred + (size_t)(TM_NT / 32) * NVM;
+  double* red = wred + (size_t)(TG / 32) * NVM;
   Ctl* cs = reinterpret_cast<Ctl*>(red + NVM);
   const float* Mg = static_cast<const float*>(a.mean);
   const float* Xg = static_cast<const float*>(a.x);
 
   if (tid < PROF_N) sprof[tid] = 0;
+  if (tid < 2) {
+    s_loads[tid] = 0;
+    s_done[tid] = NG == 1 ? 1 : 0;
+  }
   const unsigned long long t_start = ptimer(), g_start = gtimer();
   // TMEM: TM_NT columns, allocated by warp 0
   if (warp == 0) {
@@ -193,17 +333,17 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 
 #define SYNC_FLOATS()                      \
   do {                                     \
-    if (tid < K) {                         \
-      sfv[0][tid] = (float)cs->y[tid];     \
-      sfv[1][tid] = (float)cs->d[tid];     \
-      sfv[2][tid] = (float)cs->v[tid];     \
-      sfv[3][tid] = (float)cs->grad[tid];  \
+    if (lt < K) {                          \
+      sfv[0][lt] = (float)cs->y[lt];       \
+      sfv[1][lt] = (float)cs->d[lt];       \
+      sfv[2][lt] = (float)cs->v[lt];       \
+      sfv[3][lt] = (float)cs->grad[lt];    \
     }                                      \
   } while (0)
 #define LOGIC(call)                                                        \
   do {                                                                     \
     const unsigned long long tl0 = (ra.prof && tid == 0) ? ptimer() : 0;   \
-    if (tid < 32) {                                                        \
+    if (lt < 32) {                                                         \
       call;                                                                \
       __syncwarp();                                                        \
       SYNC_FLOATS();                                                       \
@@ -215,10 +355,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   // first, then shared-memory ones (separate instances of the body).
   auto sweep = [&](auto&& body) {
     for (int slot = 0; slot < nst; ++slot)
-      body(slot * TM_NT + tid, TmemRows<RS>{tbase + (unsigned)(slot * QW)});
+      body(slot * TG + lt, TmemRows<RS>{tbase + (unsigned)(slot * QW)});
     for (int slot = QT; slot < nslots; ++slot) {
-      const int qi = slot * TM_NT + tid;  // rows past qcount were never loaded
-      body(qi, SmemRows<RS>{sU + (qi - QT * TM_NT), qs, qi < qcount});
+      const int qi = slot * TG + lt;  // rows past qcount were never loaded
+      body(qi, SmemRows<RS>{sU + (qi - QT * TG), qs, qi < qcount});
     }
   };
   const float omega = a.omegaf;
@@ -239,67 +379,33 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     while (gtimer() - t0 < (unsigned long long)ra.stagger_ns) __nanosleep(1000);
   }
 
-  for (int s = team; s < ra.S; s += T) {
+  int round = 0;
+  for (int s = vt; s < ra.S; s += VT, ++round) {
     if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
-    const size_t so = (size_t)s * a.np;  // this stream's plane offset
-    // ---- load this stream's slice: U (+ weights) -> TMEM / shared memory ----
-    {
-      const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
-      const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
-      for (int slot = 0; slot < nslots; ++slot) {
-        const int qi = slot * TM_NT + tid;  // row group within the slice
-        const bool ok = qi < qcount;
-        const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
-        float4 p[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + coord)) : z4;
-        const uint32_t lb = ok ? *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + pix) : 0u;
-        if (!WCOL) sL[qi] = lb;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float row[RS];
-#pragma unroll
-          for (int j = 0; j < RS; ++j) {
-            const float4 t = j < K ? p[j] : z4;
-            row[j] = e == 0 ? t.x : (e == 1 ? t.y : (e == 2 ? t.z : t.w));
-          }
-          if (WCOL)
-            row[RS - 1] = (ok && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
-          if (slot < QT) {
-            tmem_st_row<RS>(tbase + slot * QW + e * RS, row);
-          } else if (ok) {
-            float4* rp = sU + (size_t)(e * (RS / 4)) * qs + (qi - QT * TM_NT);
-#pragma unroll
-            for (int g4 = 0; g4 < RS / 4; ++g4)
-              rp[(size_t)g4 * qs] = make_float4(row[4 * g4], row[4 * g4 + 1], row[4 * g4 + 2], row[4 * g4 + 3]);
-          }
+    if (NG > 1 && ra.alt) {
+      // the groups' slice loads alternate: A0 B0 A1 B1 ... (a finished group
+      // no longer holds the other back)
+      if (lt == 0) {
+        const int o = g ^ 1, need = g == 0 ? round : round + 1;
+        long long spins = 0;
+        while (s_loads[o] < need && !s_done[o]) {
+          __nanosleep(64);
+          if (++spins > (1LL << 28)) __trap();
         }
       }
-      tmem_wait_st();
-      // Prefetch this CTA's slice of the team's next stream into L2 so that
-      // its load (and pass 0's frame / mean reads) hit L2 a round from now.
-      if (ra.prefetch && s + T < ra.S && qcount > 0 && tid < k + 3) {
-        const int sn = s + T;
-        const size_t pofs = (size_t)q0 * 4;
-        const unsigned pb = (unsigned)qcount * 16u;
-        if (tid < k)
-          prefetch_l2(static_cast<const float*>(a.U) + ((size_t)sn * k + tid) * a.np + pofs, pb);
-        else if (tid == k)
-          prefetch_l2(Xg + (size_t)sn * a.np + pofs, pb);
-        else if (tid == k + 1 && a.pipeline)
-          prefetch_l2(Mg + (size_t)sn * a.np + pofs, pb);
-        else if (tid == k + 2)
-          prefetch_l2(a.lab + (size_t)sn * a.Pp + pofs, ((unsigned)qcount * 4u + 15u) / 16u * 16u);
-      }
-      if (tid < (int)(sizeof(Ctl) / 8))
-        reinterpret_cast<double*>(cs)[tid] = __ldcg(reinterpret_cast<const double*>(a.ctl + s) + tid);
-      __syncthreads();
-      if (tid == 0) cs->no_info = rank != 0;
-      SYNC_FLOATS();
-      __syncthreads();
-      if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += ptimer() - tw0;
+      group_sync<NG>(g);
     }
+    const size_t so = (size_t)s * a.np;  // this stream's plane offset
+    // ---- the stream's control block -----------------------------------------
+    if (lt < (int)(sizeof(Ctl) / 8))
+      reinterpret_cast<double*>(cs)[lt] = __ldcg(reinterpret_cast<const double*>(a.ctl + s) + lt);
+    group_sync<NG>(g);
+    if (lt == 0) {
+      cs->no_info = rank != 0;
+      cs->t = step_size(a, cs->frame_index);  // tracker.py:99-103, off the reductions' critical path
+    }
+    SYNC_FLOATS();
+    group_sync<NG>(g);
 
     unsigned long long tph = (ra.prof && tid == 0) ? ptimer() : 0;
 #define PHASE_MARK(idx)                              \
@@ -311,11 +417,12 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     }                                                \
   } while (0)
     // ---- frame start: running statistics (pipeline.py:120-140) -------------
+    // (reads the frame only; the normalization below needs its team sum)
     const bool upd = a.pipeline && !cs->frozen && cs->frame_index < a.i_init;
     if (upd) {
       double s1 = 0.0, s2 = 0.0, nf = 0.0;
       for (int slot = 0; slot < nslots; ++slot) {
-        const int qi = slot * TM_NT + tid;
+        const int qi = slot * TG + lt;
         if (qi >= qcount) continue;
         const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float xv[4];
@@ -330,11 +437,11 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
         }
       }
-      rstage(s1, wred, 0, 3);
-      rstage(s2, wred, 1, 3);
-      rstage(nf, wred, 2, 3);
-      team_sum(ra, team, rank, wred, 3, red, epoch, sprof);
-      if (tid == 0) {
+      rstage_g(s1, wred, 0, 3, lt);
+      rstage_g(s2, wred, 1, 3, lt);
+      rstage_g(nf, wred, 2, 3, lt);
+      team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, 3, red, epoch, sprof);
+      if (lt == 0) {
         if (red[2] > 0.0) {
           cs->status = ST_NONFINITE;
           cs->t = step_size(a, cs->frame_index);
@@ -349,7 +456,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           cs->status = ST_OK;
         }
       }
-    } else if (tid == 0) {
+    } else if (lt == 0) {
       double sd = 1.0;
       if (a.pipeline) {
         sd = cs->frozen ? cs->pstd : running_std(cs);
@@ -362,7 +469,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       cs->update_stats = 0;
       cs->status = ST_OK;
     }
-    __syncthreads();
+    group_sync<NG>(g);
+    PHASE_MARK(PROF_T_STATS);
 
     // normalized frame of a row group (pipeline.py:148-156); the sweep that
     // owns this frame's running-mean update writes the mean back
@@ -399,14 +507,88 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       }
     };
 
-    if (cs->status == ST_OK) {
-      bool bad = false;
-      bool mean_pending = upd;  // running-mean update not yet written this frame
-      // ---- cold start y = U^T x (fit.py:86-87) -------------------------------
-      if (cs->frame_index == 0) {
-        float pk[K];
+    // ---- load this stream's slice: U (+ weights) -> TMEM / shared memory,
+    // fused with pass 0: r = x - U y, cost, coordinate gradient (fit.py:96-104)
+    // needs nothing but the row itself, so it runs on the rows as they arrive
+    // from HBM (the frame and mean loads overlap the basis loads).  A
+    // stream's first frame cannot fuse: its warm start y = U^T x (fit.py:86-87)
+    // is a reduction over the whole slice, so pass 0 then sweeps separately.
+    // A frame rejected by the statistics check (non-finite) loads nothing.
+    const bool frame_ok = cs->status == ST_OK;
+    const bool cold = frame_ok && cs->frame_index == 0;
+    const bool fuse = frame_ok && !cold;
+    bool bad = false;
+    bool mean_pending = upd;  // running-mean update not yet written this frame
+    double cost = 0.0;
+    float pk[K + 1];
 #pragma unroll
-        for (int j = 0; j < K; ++j) pk[j] = 0.f;
+    for (int j = 0; j <= K; ++j) pk[j] = 0.f;
+    if (frame_ok) {
+      const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
+      const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
+      for (int slot = 0; slot < nslots; ++slot) {
+        const int qi = slot * TG + lt;  // row group within the slice
+        const bool ok = qi < qcount;
+        const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
+        float4 p[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + coord)) : z4;
+        const uint32_t lb = ok ? *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + pix) : 0u;
+        if (!WCOL) sL[qi] = lb;
+        float xh[4], w[4], r[4];
+        if (fuse) xhat(qi, mean_pending, xh, bad);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          w[e] = (ok && pix + e < a.P) ? (((lb >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
+        float tc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float row[RS];
+#pragma unroll
+          for (int j = 0; j < RS; ++j) {
+            const float4 t = j < K ? p[j] : z4;
+            row[j] = e == 0 ? t.x : (e == 1 ? t.y : (e == 2 ? t.z : t.w));
+          }
+          if (WCOL) row[RS - 1] = w[e];
+          if (slot < QT) {
+            tmem_st_row<RS>(tbase + slot * QW + e * RS, row);
+          } else if (ok) {
+            float4* rp = sU + (size_t)(e * (RS / 4)) * qs + (qi - QT * TG);
+#pragma unroll
+            for (int g4 = 0; g4 < RS / 4; ++g4)
+              rp[(size_t)g4 * qs] = make_float4(row[4 * g4], row[4 * g4 + 1], row[4 * g4 + 2], row[4 * g4 + 3]);
+          }
+          if (fuse) {
+            r[e] = __fsub_rn(xh[e], dotk<K>(row, sfv[0]));
+            float tw, gg;
+            penalty_t<PM>(r[e], w[e], a, tw, gg);
+            tc += tw;
+            pk[K] += gg * gg;
+#pragma unroll
+            for (int j = 0; j < K; ++j) pk[j] += row[j] * gg;
+          }
+        }
+        if (fuse) {
+          cost += (double)tc;
+          sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
+          sD[qi] = z4;
+        }
+      }
+      tmem_wait_st();
+      if (fuse) mean_pending = false;
+      group_sync<NG>(g);  // shared-memory rows, r and u_dir visible to every warp
+      if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += ptimer() - tw0;
+    }
+    if (NG > 1 && lt == 0) s_loads[g] = round + 1;
+    tph = (ra.prof && tid == 0) ? ptimer() : 0;
+
+    if (frame_ok) {
+      // ---- cold start y = U^T x (fit.py:86-87), then pass 0 over the slice ---
+      if (cold) {
+        float pkc[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) pkc[j] = 0.f;
         sweep([&](int qi, const auto& rows) {
           float xh[4];
           xhat(qi, upd, xh, bad);
@@ -415,60 +597,53 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             float u[RS];
             rows(e, u);
 #pragma unroll
-            for (int j = 0; j < K; ++j) pk[j] += u[j] * xh[e];
+            for (int j = 0; j < K; ++j) pkc[j] += u[j] * xh[e];
           }
         });
         mean_pending = false;
-        stage_floats<K>(pk, wred, K + 1, 0);
-        rstage(bad ? 1.0 : 0.0, wred, K, K + 1);
-        team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
-        if (tid < 32) {
-          if (red[K] > 0.0) mark_nonfinite(cs, a, s, tid);
-          else if (tid < k) cs->y[tid] = red[tid];
+        stage_floats_g<K>(pkc, wred, K + 1, 0, lt);
+        rstage_g(bad ? 1.0 : 0.0, wred, K, K + 1, lt);
+        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
+        if (lt < 32) {
+          if (red[K] > 0.0) mark_nonfinite(cs, a, s, lt);
+          else if (lt < k) cs->y[lt] = red[lt];
           __syncwarp();
           SYNC_FLOATS();
         }
-        __syncthreads();
+        group_sync<NG>(g);
+        if (cs->status == ST_OK) {
+          sweep([&](int qi, const auto& rows) {
+            float xh[4], w[4], r[4];
+            xhat(qi, mean_pending, xh, bad);
+            if (!WCOL) lab_weights(qi, w);
+            float tc = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float u[RS];
+              rows(e, u);
+              if (WCOL) w[e] = u[RS - 1];
+              r[e] = __fsub_rn(xh[e], dotk<K>(u, sfv[0]));
+              float tw, gg;
+              penalty_t<PM>(r[e], w[e], a, tw, gg);
+              tc += tw;
+              pk[K] += gg * gg;
+#pragma unroll
+              for (int j = 0; j < K; ++j) pk[j] += u[j] * gg;
+            }
+            cost += (double)tc;
+            sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
+            sD[qi] = z4;
+          });
+        }
       }
-      PHASE_MARK(PROF_T_STATS);
-
-      // ---- pass 0: r = x - U y, cost, coordinate gradient (fit.py:96-104) ---
       if (cs->status == ST_OK) {
-        double cost = 0.0;
-        float pk[K + 1];
-#pragma unroll
-        for (int j = 0; j <= K; ++j) pk[j] = 0.f;
-        sweep([&](int qi, const auto& rows) {
-          float xh[4], w[4], r[4];
-          xhat(qi, mean_pending, xh, bad);
-          if (!WCOL) lab_weights(qi, w);
-          float tc = 0.f;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float u[RS];
-            rows(e, u);
-            if (WCOL) w[e] = u[RS - 1];
-            r[e] = __fsub_rn(xh[e], dotk<K>(u, sfv[0]));
-            float tw, g;
-            penalty_t<PM>(r[e], w[e], a, tw, g);
-            tc += tw;
-            pk[K] += g * g;
-#pragma unroll
-            for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
-          }
-          cost += (double)tc;
-          sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
-          sD[qi] = z4;
-        });
-        rstage(cost, wred, 0, K + 3);
-        stage_floats<K + 1>(pk, wred, K + 3, 1);
-        rstage(bad ? 1.0 : 0.0, wred, K + 2, K + 3);
-        team_sum(ra, team, rank, wred, K + 3, red, epoch, sprof);
-        LOGIC(after_pass0<K>(cs, a, s, tid, red));
-        __syncthreads();
+        rstage_g(cost, wred, 0, K + 3, lt);
+        stage_floats_g<K + 1>(pk, wred, K + 3, 1, lt);
+        rstage_g(bad ? 1.0 : 0.0, wred, K + 2, K + 3, lt);
+        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, K + 3, red, epoch, sprof);
+        LOGIC(TM_AFTER_PASS0<K>(cs, a, s, lt, red));
+        group_sync<NG>(g);
       }
-    } else {
-      PHASE_MARK(PROF_T_STATS);
     }
     PHASE_MARK(PROF_T_PASS0);
 
@@ -512,9 +687,9 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
         });
 #pragma unroll
-        for (int m = 0; m < LSW; ++m) rstage((double)cst[m], wred, m, LSW);
-        team_sum(ra, team, rank, wred, LSW, red, epoch, sprof);
-        LOGIC(after_lsfb(cs, a, s, tid, red, base));
+        for (int m = 0; m < LSW; ++m) rstage_g((double)cst[m], wred, m, LSW, lt);
+        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, LSW, red, epoch, sprof);
+        LOGIC(TM_AFTER_LSFB(cs, a, s, lt, red, base));
       } else if (cs->need_gradfb) {
         const float al = (float)cs->acc_alpha;
         float pk[K + 1];
@@ -537,9 +712,9 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             for (int j = 0; j < K; ++j) pk[j] += u[j] * g;
           }
         });
-        stage_floats<K + 1>(pk, wred, K + 1, 0);
-        team_sum(ra, team, rank, wred, K + 1, red, epoch, sprof);
-        LOGIC(after_gradfb<K>(cs, a, s, tid, red));
+        stage_floats_g<K + 1>(pk, wred, K + 1, 0, lt);
+        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
+        LOGIC(TM_AFTER_GRADFB<K>(cs, a, s, lt, red));
       } else {
         constexpr int NV = WC + WG * (K + 1);
         const int wlo = cs->gwin_lo;
@@ -560,66 +735,73 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #pragma unroll
         for (int i = 0; i < WG * (K + 1); ++i) pk[i] = 0.f;
         // trial costs for every window step; the gradient only for the
-        // speculative pair [WLO, WLO + WG) (same arithmetic as penalty_t)
-        auto iter_sweep = [&](auto wlo_c) {
-          constexpr int WLO = decltype(wlo_c)::value;
-          sweep([&](int qi, const auto& rows) {
-            float r[4], w[4], udo[4], ud[4];
-            f4(sR[qi], r);
-            f4(sD[qi], udo);
-            if (!WCOL) lab_weights(qi, w);
+        // speculative pair [wlo, wlo + WG).  One code path: every trial value
+        // is computed once, and the pair is picked with a warp-uniform index
+        // (separate instantiations per window position were merged by the
+        // compiler into a predicated body that recomputed the trials: 12
+        // instead of 8 MUFU and ~30 selects per row).
+        static_assert(WC <= 4 && WG <= 2 && WC - WG <= 2, "window positions");
+        const bool w1 = wlo >= 1, w2 = wlo >= 2;
+        const unsigned long long tsw0 = (ra.prof && tid == 0) ? ptimer() : 0;
+        sweep([&](int qi, const auto& rows) {
+          float r[4], w[4], udo[4], ud[4];
+          f4(sR[qi], r);
+          f4(sD[qi], udo);
+          if (!WCOL) lab_weights(qi, w);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float u[RS];
-              rows(e, u);
-              if (WCOL) w[e] = u[RS - 1];
-              r[e] = trial(r[e], pa, udo[e]);  // pending accepted step (exact no-op at 0)
-              const float d = dotk<K>(u, sfv[1]);
-              ud[e] = d;
-              float gs[WG];
+          for (int e = 0; e < 4; ++e) {
+            float u[RS];
+            rows(e, u);
+            if (WCOL) w[e] = u[RS - 1];
+            r[e] = trial(r[e], pa, udo[e]);  // pending accepted step (exact no-op at 0)
+            const float d = dotk<K>(u, sfv[1]);
+            ud[e] = d;
+            float gm[WC];
 #pragma unroll
-              for (int m = 0; m < WC; ++m) {
-                const float t = trial(r[e], al[m], d);
-                if (PM == PM_HALF) {
-                  const float b = fmaf(t, t, a.muf);
-                  const float h = rsqrtf(b);
-                  const float q = rsqrtf(h);
-                  cst[m] += q * w[e];
-                  if (m >= WLO && m < WLO + WG) gs[m - WLO] = 0.5f * t * (q * w[e]) * (h * h);
-                } else {
-                  float tw, g;
-                  penalty_t<PM>(t, w[e], a, tw, g);
-                  cst[m] += tw;
-                  if (m >= WLO && m < WLO + WG) gs[m - WLO] = g;
-                }
-              }
-#pragma unroll
-              for (int mm = 0; mm < WG; ++mm) {
-                pk[mm * (K + 1) + K] += gs[mm] * gs[mm];
-#pragma unroll
-                for (int j = 0; j < K; ++j) pk[mm * (K + 1) + j] += u[j] * gs[mm];
+            for (int m = 0; m < WC; ++m) {
+              const float t = trial(r[e], al[m], d);
+              if (PM == PM_HALF) {
+                const float b = fmaf(t, t, a.muf);
+                const float h = rsqrtf(b);
+                const float q = rsqrtf(h);
+                cst[m] = fmaf(q, w[e], cst[m]);
+                gm[m] = 0.5f * t * (q * w[e]) * (h * h);
+              } else {
+                float tw, gg;
+                penalty_t<PM>(t, w[e], a, tw, gg);
+                cst[m] += tw;
+                gm[m] = gg;
               }
             }
-            sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
-            sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
-          });
-        };
-        static_assert(WC - WG <= 4, "window positions");
-        switch (wlo) {
-          case 0: iter_sweep(IC<0>{}); break;
-          case 1: iter_sweep(IC<(1 <= WC - WG ? 1 : 0)>{}); break;
-          case 2: iter_sweep(IC<(2 <= WC - WG ? 2 : 0)>{}); break;
-          case 3: iter_sweep(IC<(3 <= WC - WG ? 3 : 0)>{}); break;
-          default: iter_sweep(IC<(4 <= WC - WG ? 4 : 0)>{}); break;
-        }
-        if (tid == 0) cs->pend_alpha = 0.0;  // consumed by this sweep
+            float gs[WG];
+            gs[0] = w2 ? gm[2 < WC ? 2 : WC - 1] : (w1 ? gm[1] : gm[0]);
+            if (WG > 1) gs[WG - 1] = w2 ? gm[3 < WC ? 3 : WC - 1] : (w1 ? gm[2 < WC ? 2 : WC - 1] : gm[1]);
 #pragma unroll
-        for (int m = 0; m < WC; ++m) rstage((double)cst[m], wred, m, NV);
-        stage_floats<WG * (K + 1)>(pk, wred, NV, WC);
-        team_sum(ra, team, rank, wred, NV, red, epoch, sprof);
-        LOGIC(after_iter<K>(cs, a, s, tid, red, wlo));
+            for (int mm = 0; mm < WG; ++mm) {
+              pk[mm * (K + 1) + K] = fmaf(gs[mm], gs[mm], pk[mm * (K + 1) + K]);
+#pragma unroll
+              for (int j = 0; j < K; ++j) pk[mm * (K + 1) + j] = fmaf(u[j], gs[mm], pk[mm * (K + 1) + j]);
+            }
+          }
+          sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
+          sD[qi] = make_float4(ud[0], ud[1], ud[2], ud[3]);
+        });
+        if (lt == 0) cs->pend_alpha = 0.0;  // consumed by this sweep
+#pragma unroll
+        for (int m = 0; m < WC; ++m) rstage_g((double)cst[m], wred, m, NV, lt);
+        stage_floats_g<WG * (K + 1)>(pk, wred, NV, WC, lt);
+        if (ra.prof) {  // (uniform: every thread of the group takes the barrier)
+          const unsigned long long t1 = tid == 0 ? ptimer() : 0;
+          group_sync<NG>(g);
+          if (tid == 0) {
+            sprof[PROF_SW_OWN] += t1 - tsw0;
+            sprof[PROF_SW_ALL] += ptimer() - tsw0;
+          }
+        }
+        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
+        LOGIC(TM_AFTER_ITER<K>(cs, a, s, lt, red, wlo));
       }
-      __syncthreads();
+      group_sync<NG>(g);
     }
     PHASE_MARK(PROF_T_ITER);
 
@@ -633,9 +815,19 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       const float inv_ln = geo ? (float)(1.0 / cs->geo_ln) : 0.f;  // s = pi(eta) / ||pi(eta)||
       const float pa = (float)cs->pend_alpha;
       float* Ug = static_cast<float*>(a.U) + (size_t)s * k * a.np;
+      // r' = x - U'y (tracker.py:146) without re-reading the frame: every row
+      // moves by U'_i - U_i = coef_i v^T with v = y / ||y||, so
+      // U'_i y = U_i y + coef_i ||y|| and r'_i = r_i - coef_i ||y||, where r is
+      // the fit residual x - U y kept on chip (fit.py's res, the same
+      // recurrence of accepted steps as the reference)
+      const float yn = (float)cs->geo_yn;
+      const bool want_bg = a.bg_out != nullptr;
       sweep([&](int qi, const auto& rows) {
         const bool ok = qi < qcount;
         const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
+        const size_t off = so + coord;
+        float m4[4] = {0.f, 0.f, 0.f, 0.f};  // running mean for the background, loaded first
+        if (want_bg && a.pipeline && ok && !qr) f4(*reinterpret_cast<const float4*>(Mg + off), m4);
         float r[4], w[4], ud[4];
         f4(sR[qi], r);
         f4(sD[qi], ud);
@@ -657,6 +849,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             const float ug = dotk<K>(u, sfv[3]);
             coef = ga * uv - gsn * ((eta - ug) * inv_ln);
           }
+          rr[e] = fmaf(-coef, yn, r[e]);
 #pragma unroll
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
         }
@@ -669,18 +862,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
                      make_float4(up[0][j], up[1][j], up[2][j], up[3][j]));
         }
         if (qr) return;
-        const size_t off = so + coord;
-        // r' = x - U'y from the frame (tracker.py:146), as the reference orders it
-        float xh[4], bgn[4];
-        bool bad_unused = false;
-        xhat(qi, false, xh, bad_unused);
         uint32_t nl = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          bgn[e] = dotk<K>(up[e], sfv[0]);
-          rr[e] = __fsub_rn(xh[e], bgn[e]);
+        for (int e = 0; e < 4; ++e)
           if (pix + e < a.P && fabsf(rr[e]) >= a.deltaf) nl |= 1u << (8 * e);
-        }
         if (a.C == 1) {
           *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
           if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
@@ -689,37 +874,39 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         }
         if (a.res_out)
           *reinterpret_cast<float4*>(static_cast<float*>(a.res_out) + off) = make_float4(rr[0], rr[1], rr[2], rr[3]);
-        if (a.bg_out) {
+        if (want_bg) {
           const float sc = (float)cs->std_cur;
-          float m4[4], b[4];
-          f4(a.pipeline ? *reinterpret_cast<const float4*>(Mg + off) : z4, m4);
+          float b[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
+          for (int e = 0; e < 4; ++e) {
+            const float bgn = dotk<K>(up[e], sfv[0]);  // U'y
+            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn * sc, m4[e]), 0.f), 1.f) : bgn;
+          }
           *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + off) = make_float4(b[0], b[1], b[2], b[3]);
         }
       });
     }
 
     // ---- commit the control block (one writer per stream) ------------------
-    __syncthreads();
+    group_sync<NG>(g);
     PHASE_MARK(PROF_T_GEO);
 #undef PHASE_MARK
-    if (tid == 0) cs->pend_alpha = 0.0;
-    __syncthreads();
-    if (rank == 0 && tid < (int)(sizeof(Ctl) / 8))
-      reinterpret_cast<double*>(a.ctl + s)[tid] = reinterpret_cast<const double*>(cs)[tid];
-    __syncthreads();
+    if (lt == 0) cs->pend_alpha = 0.0;
+    group_sync<NG>(g);
+    if (rank == 0 && lt < (int)(sizeof(Ctl) / 8))
+      reinterpret_cast<double*>(a.ctl + s)[lt] = reinterpret_cast<const double*>(cs)[lt];
+    group_sync<NG>(g);
   }
+  if (NG > 1 && lt == 0) s_done[g] = 1;
 #undef LOGIC
 #undef SYNC_FLOATS
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
   if (ra.prof && tid == 0) {
     sprof[PROF_TOTAL] = ptimer() - t_start;
     sprof[PROF_GT_TOTAL] = gtimer() - g_start;
     for (int i = 0; i < PROF_N; ++i) ra.prof[(size_t)blockIdx.x * PROF_N + i] = sprof[i];
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tbase), "n"(TM_NT));
 }

@@ -112,6 +112,15 @@ class ShardedTracker:
         return full[self.row0 * W: self.row1 * W]
 
     # -- collectives ------------------------------------------------------------
+    def _on(self, cuda_stream: int):
+        """Run the collectives on the CUDA stream the phase kernels use, so the
+        all-reduce is ordered after the kernels that fill the exchange buffer
+        and before the one that consumes it."""
+        torch = self.torch
+        if cuda_stream == 0:
+            return torch.cuda.stream(torch.cuda.default_stream(self.device))
+        return torch.cuda.stream(torch.cuda.ExternalStream(cuda_stream, device=self.device))
+
     def _allreduce(self, t):
         if self.world == 1:
             return
@@ -140,13 +149,15 @@ class ShardedTracker:
         nt.xbegin(block, background=background, residual=residual, mask=mask, raw_mask=raw_mask,
                   fit=fit, cuda_stream=cuda_stream)
         while nt.xnext(cuda_stream):
-            self._allreduce(self.xred)
+            with self._on(cuda_stream):
+                self._allreduce(self.xred)
             self.exchanges += 1
             nt.xapply(cuda_stream)
         halo_top = halo_bot = None
         if mask is not None and self.world > 1:
             nt.xedges(self.edges[0].data_ptr(), self.edges[1].data_ptr(), cuda_stream)
-            self._allgather_edges()
+            with self._on(cuda_stream):
+                self._allgather_edges()
             if self.rank > 0:
                 halo_top = self.gathered[self.rank - 1, 1].data_ptr()
             if self.rank < self.world - 1:

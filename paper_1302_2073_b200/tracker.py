@@ -130,6 +130,26 @@ def random_orthonormal(m: int, k: int, seed: int) -> SubspaceBasis:
     return SubspaceBasis(q)
 
 
+def rewrap_fp64(state: TrackerState) -> TrackerState:
+    """Export form of an fp32 device state for the reference's types.
+
+    The fp32 basis drifts from orthonormality by ~1e-7 after some frames, and
+    the reference's `SubspaceBasis` rejects drift > 1e-8 (manifold.py:66-70),
+    so an exported basis is re-orthonormalized on the host in fp64 with the
+    reference's own QR + sign fix (manifold.py:111-112, 192-196): U = Q R,
+    diag(R) > 0.  The coordinates become R y so that the reconstruction U y
+    (the background, jobs.py:231-239) is unchanged.  The subspace, weights,
+    frame index and running statistics are carried over as they are."""
+    U = np.asarray(state.basis.data, dtype=np.float64)
+    q, r = np.linalg.qr(U)
+    sign = np.where(np.diag(r) < 0.0, -1.0, 1.0)
+    q = q * sign
+    r = sign[:, None] * r
+    y = r @ np.asarray(state.y, dtype=np.float64)
+    return TrackerState(SubspaceBasis(q, steps_since_qr=0), y, state.weights, state.frame_index,
+                        state.preproc)
+
+
 def bootstrap(m: int, params: ProstParams, seed: int) -> TrackerState:
     """Fresh state: random orthonormal basis, zero coordinates, unit weights
     (tracker.py:106-118)."""
@@ -379,7 +399,7 @@ class NativeTracker:
         d = {nm: out[i] / 1e3 for i, nm in enumerate(names)}
         d.update(team_sums=int(out[5]), rounds=int(out[6]), slowest_kernel_us=out[n - 1] / 1e3)
         for i, nm in ((7, "phase_stats_us"), (8, "phase_pass0_us"), (9, "phase_iter_us"),
-                      (10, "phase_geo_us")):
+                      (10, "phase_geo_us"), (12, "iter_sweep_own_us"), (13, "iter_sweep_all_us")):
             d[nm] = out[i] / 1e3
         return d
 
@@ -556,7 +576,10 @@ class StreamTracker:
 
         if self._native is None:
             raise ConfigError("no frames pushed yet; nothing to snapshot")
-        return pack_snapshot(self.state, self.params)
+        state = self.state
+        if self.precision != "fp64":
+            state = rewrap_fp64(state)
+        return pack_snapshot(state, self.params)
 
     def save(self, path) -> None:
         with open(path, "wb") as fh:

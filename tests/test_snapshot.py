@@ -76,3 +76,46 @@ def test_restore_continues_like_reference(precision):
         assert worst_mask == 0.0 and worst_bg <= 1e-9
     else:
         assert worst_mask <= 1e-3 and worst_bg <= 1e-4
+
+
+@pytest.mark.gpu
+def test_fp32_export_is_accepted_by_reference_types():
+    """A snapshot of an fp32 tracker after 220 frames: its basis passes the
+    reference's orthonormality check (drift <= 1e-8, manifold.py:66-70; fp32
+    drift alone is ~1e-7), and the oracle continued from the blob tracks the
+    GPU tracker that wrote it (SURVEY.md §8(b) export rule)."""
+    from oracle import prost_oracle as orc
+    from paper_1302_2073_b200.synth import SceneSpec, SceneStream
+
+    W, H = 64, 48
+    cfg = pkg.RunConfig(subspace_dim=8, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=50, seed=3)
+    frames = SceneStream(SceneSpec(width=W, height=H, rank=4, seed=7)).next_frames(226)
+    tr = pkg.StreamTracker(cfg, precision="fp32")
+    for v in frames[:220]:
+        tr.push(pkg.FrameBuffer(W, H, 1, v))
+    raw_drift = np.linalg.norm(tr.state.basis.data.T @ tr.state.basis.data - np.eye(8))
+    blob = tr.snapshot_bytes()
+    params = cfg.params(50)
+    U, y, w, fi, pre = unpack_snapshot(blob, params)
+    drift = np.linalg.norm(U.T @ U - np.eye(8))
+    print(f"fp32 drift {raw_drift:.2e} -> exported {drift:.2e}")
+    assert drift <= 1e-8
+    SubspaceBasis(U)  # the reference's check (raises DimensionError above 1e-8)
+    assert fi == 220 and pre is not None and pre.frozen
+    # the reconstruction is unchanged by the re-wrap
+    bg_gpu = tr.background_frame().data
+    o = orc.PipelineOracle(W, H, 1, orc.OracleParams(
+        k=8, p=0.5, mu=1e-4, delta=params.delta, omega=params.omega, t_init=params.t_init,
+        t_min=params.t_min, tau=params.tau, max_iters=2), i_init=50, seed=3)
+    o.norm = orc.Normalizer(pre.mean.copy(), pre.frames_seen, pre.frozen, pre.std, pre.value_sum,
+                            pre.value_sumsq, pre.value_count)
+    o.state = orc.CoreState(U, y, w, fi, 0)
+    assert np.linalg.norm(o.background() - bg_gpu) <= 1e-6 * np.linalg.norm(bg_gpu)
+    for v in frames[220:]:
+        a = tr.push(pkg.FrameBuffer(W, H, 1, v))
+        b = o.push(v)
+        assert np.mean(a.mask.labels != b.mask) <= 1e-3
+    bg = tr.background_frame().data
+    assert np.linalg.norm(bg - o.background()) <= 1e-4 * np.linalg.norm(o.background())
+    assert orc.subspace_sine(tr.state.basis.data, o.state.U) <= 1e-3
