@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PROST_ABI_VERSION 1
+#define PROST_ABI_VERSION 2
 
 /* status codes (errors.py:14-39) */
 #define PROST_OK 0
@@ -101,6 +101,8 @@ typedef struct prost_outputs {
   prost_fit_info* fit;    /* HOST array [n_streams]; non-NULL makes the call synchronous */
   int32_t dtype;          /* PROST_F32 or PROST_F64 for background/residual */
   int32_t on_device;      /* 1: the array pointers above are device pointers */
+  void* fit_residual;     /* x - U y after the fit, before the geodesic (FitResult.residual,
+                             fit.py:50-63); same dtype / placement as background */
 } prost_outputs;
 
 typedef struct prost_handle prost_handle;

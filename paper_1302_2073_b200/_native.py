@@ -71,7 +71,7 @@ class Outputs(ctypes.Structure):
         ("background", ctypes.c_void_p), ("residual", ctypes.c_void_p),
         ("mask", ctypes.c_void_p), ("raw_mask", ctypes.c_void_p),
         ("fit", ctypes.POINTER(FitInfo)), ("dtype", ctypes.c_int32),
-        ("on_device", ctypes.c_int32),
+        ("on_device", ctypes.c_int32), ("fit_residual", ctypes.c_void_p),
     ]
 
 
@@ -122,7 +122,7 @@ def lib() -> ctypes.CDLL:
     for name in EXPORTS:
         if name not in ("prost_destroy",):
             getattr(L, name).restype = ctypes.c_int
-    if L.prost_abi_version() != 1:
+    if L.prost_abi_version() != 2:
         raise ImportError("libprost_b200.so ABI version mismatch")
     _lib = L
     return L

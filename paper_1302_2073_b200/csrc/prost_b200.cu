@@ -85,6 +85,7 @@ struct prost_handle {
   // lazily allocated
   void* bgbuf = nullptr;
   void* resbuf = nullptr;
+  void* fresbuf = nullptr;  // fit residual (FitResult.residual) when it cannot be written in place
   uint8_t* maskbuf = nullptr;
   // conversion staging: uploads (frames) and downloads (outputs) have their
   // own buffers, so a pipelined push's upload of frame N+1 on s_in never
@@ -520,7 +521,14 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   const bool same = (dtype == PROST_F64) == h->fp64 && dtype != PROST_U8;
   const bool dense = h->P == h->Pp;
   const void* xdev = h->x;
-  if (on_device && same && dense) {
+  // 8-bit frames go to the TMEM kernel as they are (1 byte per coordinate in
+  // HBM and over PCIe) and are divided by 255 on load; the other kernels read
+  // a converted copy (k_pack)
+  const bool x8 = dtype == PROST_U8 && h->tmem && dense;
+  if (x8) {
+    if (on_device) xdev = frames;
+    else CK(cudaMemcpyAsync(h->x, frames, (size_t)h->S * h->C * h->P, cudaMemcpyHostToDevice, st));
+  } else if (on_device && same && dense) {
     xdev = frames;  // zero-copy: kernels read the caller's device frames
   } else {
     int rc = upload_dense(h, frames, dtype, on_device, h->x, h->S * h->C, st);
@@ -534,6 +542,15 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   cudaError_t e = cudaSuccess;
   Args a = make_args(h, 0);
   a.x = xdev;
+  a.xu8 = x8 ? 1 : 0;
+  if (o.fit_residual) {
+    if (o.on_device && osame && dense) a.fitres_out = o.fit_residual;
+    else {
+      if (!h->fresbuf) h->fresbuf = dev_alloc(fbytes, &e);
+      if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "fit residual buffer: %s", cudaGetErrorString(e));
+      a.fitres_out = h->fresbuf;
+    }
+  }
   if (o.background) {
     if (o.on_device && osame && dense) a.bg_out = o.background;
     else {
@@ -575,6 +592,8 @@ int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStr
     rc = download_dense(h, h->bgbuf, o.background, odt, o.on_device, h->S * h->C, st);
   if (!rc && o.residual && a.res_out == h->resbuf)
     rc = download_dense(h, h->resbuf, o.residual, odt, o.on_device, h->S * h->C, st);
+  if (!rc && o.fit_residual && a.fitres_out == h->fresbuf)
+    rc = download_dense(h, h->fresbuf, o.fit_residual, odt, o.on_device, h->S * h->C, st);
   if (!rc && o.mask && a.mask_out == h->maskbuf) rc = copy_labels(h, h->maskbuf, o.mask, o.on_device, st);
   if (!rc && o.raw_mask && a.raw_out == nullptr) rc = copy_labels(h, h->lab, o.raw_mask, o.on_device, st);
   if (rc) return rc;
@@ -934,7 +953,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
 void prost_destroy(prost_handle* h) {
   if (!h) return;
   void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
-                  h->rinv, h->info, h->bgbuf, h->resbuf, h->maskbuf, h->stage[0], h->stage[1],
+                  h->rinv, h->info, h->bgbuf, h->resbuf, h->fresbuf, h->maskbuf, h->stage[0], h->stage[1],
                   h->rbar, h->rpart, h->rprof, h->xred, h->xgo, h->labc};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1124,7 +1143,7 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   const char* nopipe = getenv("PROST_NO_PIPE");
   // (raw labels are copied from the label state itself, which the next frame's
   // kernels overwrite: no pipelining when they are requested)
-  if (!on_device && out && !out->on_device && !out->fit && !out->raw_mask && !h->prof &&
+  if (!on_device && out && !out->on_device && !out->fit && !out->raw_mask && !out->fit_residual && !h->prof &&
       !(nopipe && nopipe[0] == '1'))
     return push_pipelined(h, frames, dtype, out, st);
   if (h->io_pending) {  // order after the pipelined pushes before this one

@@ -97,6 +97,7 @@ struct Args {
   FitInfo* info;       // [S]
   void* bg_out;        // [S][np] or null
   void* res_out;       // [S][np] or null
+  void* fitres_out;    // [S][np] fit residual x - U y before the geodesic (FitResult.residual) or null
   uint8_t* raw_out;    // [S][Pp] or null
   uint8_t* mask_out;   // [S][Pp] or null
   // Pixel-sharded (exchange) mode: a phase kernel's last CTA leaves the
@@ -108,6 +109,7 @@ struct Args {
   const uint8_t* halo_top;  // [S][width] label row above the local rows, or null
   const uint8_t* halo_bot;  // [S][width] label row below the local rows, or null
   uint8_t* labc;       // [S][np] per-coordinate flags of the TMEM kernel (3 channels), or null
+  int xu8;             // TMEM kernel: x holds 8-bit frames, divided by 255 on load (frameio.py:136)
   int s0;              // first stream of this launch
   int k, C, P, Pp, width, height;
   long long np;        // padded coordinates per stream = C * Pp

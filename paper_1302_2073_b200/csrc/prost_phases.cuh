@@ -31,9 +31,14 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 template <typename T, int VEC>
 __device__ __forceinline__ void normalized(const Args& a, size_t off, bool upd, bool wr, T seen,
                                            T stdv, T (&xh)[VEC], bool& bad) {
-  const T* X = static_cast<const T*>(a.x) + off;
   T xv[VEC];
-  VecIO<T, VEC>::ldg(X, xv);
+  if (a.xu8) {  // 8-bit frames (TMEM path; the periodic-QR relabel reads them too)
+    const uint8_t* X8 = static_cast<const uint8_t*>(a.x) + off;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) xv[e] = (T)((double)X8[e] * (1.0 / 255.0));
+  } else {
+    VecIO<T, VEC>::ldg(static_cast<const T*>(a.x) + off, xv);
+  }
 #pragma unroll
   for (int e = 0; e < VEC; ++e) bad |= !isfinite(xv[e]);
   if (!a.pipeline) {
@@ -622,6 +627,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_geo(const __grid_constant__ 
   uint8_t* L = a.lab + (size_t)s * a.Pp;
   T* BG = a.bg_out ? static_cast<T*>(a.bg_out) + (size_t)s * a.np : nullptr;
   T* RES = a.res_out ? static_cast<T*>(a.res_out) + (size_t)s * a.np : nullptr;
+  T* FRES = (!QR && a.fitres_out) ? static_cast<T*>(a.fitres_out) + (size_t)s * a.np : nullptr;
   for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
     const int pix = q * VEC;
     T w[VEC];
@@ -631,6 +637,16 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_geo(const __grid_constant__ 
     for (int e = 0; e < VEC; ++e) mx[e] = (T)0;
     for (int ch = 0; ch < a.C; ++ch) {
       const size_t off = (size_t)ch * a.Pp + pix;
+      if (FRES) {  // FitResult.residual: x - U y after the fit (fit.py:50-63)
+        T r[VEC], ud[VEC];
+        VecIO<T, VEC>::ld(R + off, r);
+        if (sc[3] != 0.0) {
+          VecIO<T, VEC>::ld(UD + off, ud);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) r[e] = trial(r[e], pend, ud[e]);
+        }
+        VecIO<T, VEC>::st(FRES + off, r);
+      }
       T u[K][VEC];
 #pragma unroll
       for (int j = 0; j < K; ++j) {

@@ -551,6 +551,9 @@ __global__ void __launch_bounds__(NTMAX, 1) k_resident(const __grid_constant__ A
       }
 
       if (cs->status == ST_OK) {
+        if (a.fitres_out && own)  // FitResult.residual (fit.py:50-63)
+          *reinterpret_cast<float4*>(static_cast<float*>(a.fitres_out) + (size_t)s * a.np + pix) =
+              make_float4(r[0], r[1], r[2], r[3]);
         // ---- geodesic step of the basis (manifold.py:116-197) ---------------
         if (cs->do_geo) {
           const float ga = (float)cs->geo_a, gsn = (float)cs->geo_s, ln = (float)cs->geo_ln;

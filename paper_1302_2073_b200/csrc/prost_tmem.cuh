@@ -309,6 +309,19 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   Ctl* cs = reinterpret_cast<Ctl*>(red + NVM);
   const float* Mg = static_cast<const float*>(a.mean);
   const float* Xg = static_cast<const float*>(a.x);
+  // 4 frame values at coordinate offset off: fp32, or 8-bit divided by 255
+  // exactly as the conversion kernel k_pack does (double product, rounded)
+  auto ld_x4 = [&](size_t off, float (&xv)[4]) {
+    if (a.xu8) {
+      const uchar4 b = *reinterpret_cast<const uchar4*>(static_cast<const uint8_t*>(a.x) + off);
+      xv[0] = (float)((double)b.x * (1.0 / 255.0));
+      xv[1] = (float)((double)b.y * (1.0 / 255.0));
+      xv[2] = (float)((double)b.z * (1.0 / 255.0));
+      xv[3] = (float)((double)b.w * (1.0 / 255.0));
+    } else {
+      f4(*reinterpret_cast<const float4*>(Xg + off), xv);
+    }
+  };
 
   if (tid < PROF_N) sprof[tid] = 0;
   if (tid < 2) {
@@ -426,7 +439,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         if (qi >= qcount) continue;
         const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float xv[4];
-        f4(*reinterpret_cast<const float4*>(Xg + so + coord), xv);
+        ld_x4(so + coord, xv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (pix + e < a.P) {
@@ -479,8 +492,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     auto xhat = [&](int qi, bool wr, float (&xh)[4], bool& bad) {
       const bool ok = qi < qcount;
       const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
-      float xv[4];
-      f4(ok ? *reinterpret_cast<const float4*>(Xg + so + coord) : z4, xv);
+      float xv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (ok) ld_x4(so + coord, xv);
       if (a.pipeline) {
         float mv[4];
         f4(ok ? *reinterpret_cast<const float4*>(Mg + so + coord) : z4, mv);
@@ -839,7 +852,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           float u[RS];
           rows(e, u);
           if (WCOL) w[e] = u[RS - 1];
-          r[e] = trial(r[e], pa, ud[e]);
+          r[e] = trial(r[e], pa, ud[e]);  // the fit residual x - U y (fit.py res)
           float coef = 0.f;
           if (geo) {
             float tw, g;
@@ -854,6 +867,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
         }
         if (!ok) return;
+        if (a.fitres_out)
+          *reinterpret_cast<float4*>(static_cast<float*>(a.fitres_out) + off) = make_float4(r[0], r[1], r[2], r[3]);
         if (geo) {
 #pragma unroll
           for (int j = 0; j < K; ++j)

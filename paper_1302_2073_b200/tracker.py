@@ -105,9 +105,9 @@ class TrackerState:
 
 @dataclass
 class FitResult:
-    """fit.py:50-63.  `residual` is not read back from the device (None); the
-    residual that matters downstream — against the updated basis — is the
-    second return value of `process_frame`."""
+    """fit.py:50-63: the fitted coordinates, the residual x - U y at them
+    (before the geodesic step; the residual against the updated basis is the
+    second return value of `process_frame`), the cost and the counters."""
 
     y: np.ndarray
     residual: Optional[np.ndarray]
@@ -275,18 +275,20 @@ class NativeTracker:
 
     # -- frames --------------------------------------------------------------
     def push(self, frames, background=None, residual=None, mask=None, raw_mask=None,
-             fit: bool = True, cuda_stream: int = 0):
+             fit: bool = True, cuda_stream: int = 0, fit_residual=None):
         """Enqueue one frame per stream.  Outputs are numpy arrays or torch
         tensors (host or device) to fill.  With fit=True the call waits and
-        returns the per-stream `prost_fit_info` array."""
+        returns the per-stream `prost_fit_info` array.  `fit_residual` receives
+        x - U y after the fit, before the geodesic step (FitResult.residual)."""
         fp, fdt, fdev, out = self._frame_and_outputs(frames, background, residual, mask,
-                                                     raw_mask, fit)
+                                                     raw_mask, fit, fit_residual)
         rc = self._lib.prost_push(self._h, fp, fdt, fdev, ctypes.byref(out),
                                   ctypes.c_void_p(cuda_stream))
         self._check(rc, "push")
         return self._fit if fit else None
 
-    def _frame_and_outputs(self, frames, background, residual, mask, raw_mask, fit):
+    def _frame_and_outputs(self, frames, background, residual, mask, raw_mask, fit,
+                           fit_residual=None):
         fp, fdt, fdev, fcount = _buffer(frames)
         if fcount != self.n_streams * self.m:
             raise DimensionError(
@@ -295,6 +297,7 @@ class NativeTracker:
         dev_flags = set()
         dtype = None
         for name, arr, count in (("background", background, self.m), ("residual", residual, self.m),
+                                 ("fit_residual", fit_residual, self.m),
                                  ("mask", mask, self.pixels), ("raw_mask", raw_mask, self.pixels)):
             if arr is None:
                 continue
@@ -453,13 +456,15 @@ def process_frame(state: TrackerState, x: np.ndarray, params: ProstParams, *,
     h.set_core_state(0, basis.data, state.y, state.weights, state.frame_index,
                      basis.steps_since_qr)
     residual = np.empty(basis.m)
-    info = h.push(np.ascontiguousarray(x, dtype=np.float64), residual=residual, fit=True)[0]
+    fit_res = np.empty(basis.m)
+    info = h.push(np.ascontiguousarray(x, dtype=np.float64), residual=residual, fit=True,
+                  fit_residual=fit_res)[0]
     U, y, w, fi, since = h.get_core_state(0)
     new_state = TrackerState(
         basis=SubspaceBasis(U, steps_since_qr=since, check=False),
         y=y, weights=w, frame_index=fi, preproc=state.preproc,
     )
-    fit = FitResult(y=y.copy(), residual=None, cost=info.fit_cost, iterations=info.iterations,
+    fit = FitResult(y=y.copy(), residual=fit_res, cost=info.fit_cost, iterations=info.iterations,
                     cost_evals=info.cost_evals, grad_evals=info.grad_evals)
     return new_state, residual, fit
 

@@ -231,3 +231,42 @@ def test_c4_row_block_exchange_program_teacher_forced():
               (info.iterations, info.cost_evals) == (r.fit.iterations, r.fit.cost_evals),
               r.fit.armijo_margin)
     assert_tf(w)
+
+
+def test_u8_frames_against_oracle():
+    """8-bit frames read by the TMEM kernel itself (1 byte per coordinate,
+    divided by 255 on load like frameio.py:136) against the oracle fed
+    frame / 255 in float64: C0 shape, 30 frames free running (within the
+    self-divergence horizon), teacher-forced tolerances on the first frames."""
+    import torch
+
+    from paper_1302_2073_b200 import _native as nat
+    from parity import Worst, oracle_for
+    from paper_1302_2073_b200.synth import CONFIGS
+
+    cfg = pkg.RunConfig(i_init=10, **CONFIGS["C0"]["tracker"])
+    W, H = cfg.target_width, cfg.target_height
+    from paper_1302_2073_b200.synth import SceneStream, config_spec
+
+    frames = SceneStream(config_spec("C0", 0)).next_frames(30)
+    q = np.clip(np.rint(frames * 255.0), 0, 255).astype(np.uint8)
+    bt = pkg.BatchTracker(cfg, 1, seeds=[0], latency=True)
+    assert bt.native.query(nat.Q_RESIDENT) == 2
+    o = oracle_for(cfg, 10, W, H, 1, 0)
+    mask = torch.empty((1, W * H), dtype=torch.uint8, device="cuda")
+    bg = torch.empty((1, W * H), dtype=torch.float32, device="cuda")
+    w_free = Worst()
+    from oracle import prost_oracle as orc
+
+    for t in range(30):
+        info = bt.push(torch.from_numpy(q[t][None]).cuda(), background=bg, mask=mask, fit=True)[0]
+        r = o.push(q[t].astype(np.float64) / 255.0)
+        rb = o.background()
+        w_free.add(t, 0, orc.subspace_sine(bt.native.get_core_state(0)[0], o.state.U),
+                   float(np.linalg.norm(bg.cpu().numpy()[0] - rb) / np.linalg.norm(rb)), 0.0,
+                   float(np.mean(mask.cpu().numpy()[0] != r.mask)),
+                   abs(info.fit_cost - r.fit_cost) / abs(r.fit_cost),
+                   (info.iterations, info.cost_evals) == (r.fit.iterations, r.fit.cost_evals),
+                   r.fit.armijo_margin)
+    print(w_free)
+    assert w_free.bg_rel <= 1e-4 and w_free.sine <= 1e-3 and w_free.mask <= 1e-3

@@ -56,6 +56,12 @@ def test_process_frame_teacher_forced(precision):
         st = pkg.TrackerState(pkg.SubspaceBasis(U_prev), y_prev, w_prev, frame_index=i)
         new, r, fit = pkg.process_frame(st, x, params, precision=precision)
         assert new.frame_index == i + 1
+        oprm = orc.OracleParams(k=params.k, p=params.cfg.p, mu=params.cfg.mu, delta=params.delta,
+                                omega=params.omega, t_init=params.t_init, t_min=params.t_min,
+                                tau=params.tau, max_iters=params.cg.max_iters)
+        ofit = orc.fit(U_prev, x, None if i == 0 else y_prev, oprm, w_prev)
+        np.testing.assert_allclose(fit.residual, ofit.residual, rtol=0,
+                                   atol=1e-9 if precision == "fp64" else 1e-4)
         same = [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z["counts"][i])
         same_counts += same
         if precision == "fp64":
@@ -105,6 +111,9 @@ def test_fit_cases(precision):
         _, _, fit = pkg.process_frame(st, z[key + "x"], params, precision=precision)
         tol = 1e-10 if precision == "fp64" else 2e-4
         np.testing.assert_allclose(fit.y, z[key + "y"], rtol=tol, atol=tol)
+        # FitResult.residual: x - U y at the fitted coordinates (fit.py:50-63)
+        np.testing.assert_allclose(fit.residual, z[key + "residual"], rtol=0,
+                                   atol=1e-9 if precision == "fp64" else 2e-4)
         assert fit.cost == pytest.approx(float(z[key + "cost"]), rel=tol)
         if precision == "fp64":
             assert [fit.iterations, fit.cost_evals, fit.grad_evals] == list(z[key + "counts"])
