@@ -53,6 +53,12 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=12, help="oracle frames per CPU worker")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-port", action="store_true",
+                    help="also time the numpy port beside the reference package (their ratio)")
+    ap.add_argument("--e2e-background", action="store_true",
+                    help="the end-to-end leg also downloads every stream's background frame")
+    ap.add_argument("--e2e-f32", action="store_true",
+                    help="end-to-end leg with fp32 frames instead of 8-bit camera frames")
     ap.add_argument("--wave", type=int, default=0)
     ap.add_argument("--pixel-shard", action="store_true",
                     help="shard one stream's pixel rows over the ranks (default for C4 with N > 1)")
@@ -151,47 +157,74 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port, one stream per worker process
+# CPU baseline: the reference's own StreamTracker (baseline/_ref, the unmodified
+# package installed offline) — or, when that install is absent, the numpy port
+# of its path (oracle/, pinned bit-exact to it) — one stream per worker process,
+# timed on the same steady-state frame window as the GPU arm (after the i_init
+# statistics window, which is pushed untimed first).
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _reference_tracker(tracker, i_init, kind):
+    """A StreamTracker-like object with push(vec) for the CPU arm."""
+    W, H = tracker["target_width"], tracker["target_height"]
+    ch = 1 if tracker["grayscale"] else 3
+    if kind == "reference":
+        if str(REF_DIR) not in sys.path:
+            sys.path.insert(0, str(REF_DIR))
+        from prost import jobs, pipeline  # the reference package itself
+
+        tr = jobs.StreamTracker(jobs.RunConfig(**tracker), i_init=i_init)
+        return lambda v: tr.push(pipeline.FrameBuffer(W, H, ch, v))
+    from oracle import prost_oracle as orc
+    from paper_1302_2073_b200.params import RunConfig
+
+    prm = RunConfig(**tracker).params(i_init)
+    ref = orc.PipelineOracle(W, H, ch, orc.OracleParams(
+        k=prm.k, p=prm.cfg.p, mu=prm.cfg.mu, delta=prm.delta, omega=prm.omega,
+        t_init=prm.t_init, t_min=prm.t_min, tau=prm.tau, max_iters=prm.cg.max_iters),
+        i_init=i_init, seed=RunConfig(**tracker).seed)
+
+    def push(v):
+        ref.push(v)
+        ref.background()
+    return push
 
 
 def _cpu_worker(job):
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    name, sid, n_frames, tracker = job
+    name, sid, n_frames, tracker, kind, preroll = job
     sys.path.insert(0, str(ROOT))
-    from oracle import prost_oracle as orc
-    from paper_1302_2073_b200.params import RunConfig
-
-    frames = gen_frames(name, [sid], n_frames + 1, dtype=np.float64)[:, 0]
-    cfg = RunConfig(**tracker)
-    prm = cfg.params(100)
-    W, H = cfg.target_width, cfg.target_height
-    ch = 1 if cfg.grayscale else 3
-    ref = orc.PipelineOracle(W, H, ch, orc.OracleParams(
-        k=prm.k, p=prm.cfg.p, mu=prm.cfg.mu, delta=prm.delta, omega=prm.omega,
-        t_init=prm.t_init, t_min=prm.t_min, tau=prm.tau, max_iters=prm.cg.max_iters),
-        i_init=100, seed=cfg.seed)
-    ref.push(frames[0])  # bootstrap (basis QR) outside the timed part
+    frames = gen_frames(name, [sid], preroll + n_frames, dtype=np.float64)[:, 0]
+    push = _reference_tracker(tracker, 100, kind)
+    for f in frames[:preroll]:  # the statistics window, untimed (the GPU arm's pre-roll)
+        push(f)
     t0 = time.perf_counter()
-    for f in frames[1:]:
-        ref.push(f)
-        ref.background()
+    for f in frames[preroll:]:
+        push(f)
     return n_frames, time.perf_counter() - t0
 
 
-def cpu_rate(name, tracker, n_frames, cores=None):
+def reference_kind():
+    return "reference" if (REF_DIR / "prost" / "jobs.py").exists() else "port"
+
+
+def cpu_rate(name, tracker, n_frames, cores=None, kind=None, preroll=100):
     import multiprocessing as mp
 
     cores = cores or len(os.sched_getaffinity(0))
+    kind = kind or reference_kind()
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
-    jobs = [(name, sid, n_frames, tracker) for sid in range(cores)]
+    jobs = [(name, sid, n_frames, tracker, kind, preroll) for sid in range(cores)]
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
         res = pool.map(_cpu_worker, jobs)
     wall = time.perf_counter() - t0
     frames = sum(r[0] for r in res)
     slowest = max(r[1] for r in res)
-    return frames / slowest, cores, frames, wall
+    return frames / slowest, cores, frames, wall, kind
 
 
 def cpu_model():
@@ -239,9 +272,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = len(os.sched_getaffinity(0))
-    # each step: one frame for `cores` streams (one worker process each)
+    # each step: one frame for `cores` streams (one worker process each), on
+    # the GPU arm's steady-state window (the statistics window is pre-rolled)
     n_frames = args.warmup + args.steps
-    rate, cores, frames, wall = cpu_rate(args.config, tracker, n_frames, cores)
+    rate, cores, frames, wall, kind = cpu_rate(args.config, tracker, n_frames, cores)
     W, H = tracker["target_width"], tracker["target_height"]
     P = W * H
     line = {
@@ -254,9 +288,11 @@ def run_reference(args):
                    "streams_per_step": cores},
         "mpix_per_s": rate * P / 1e6,
         "cpu_baseline": {"value": rate, "unit": "stream-frames/s", "cores": cores,
-                         "kind": "port", "cpu": cpu_model(),
+                         "kind": kind, "cpu": cpu_model(),
                          "sample": f"{cores} worker processes x {n_frames} frames of their own "
-                                   f"{args.config} stream (numpy oracle, OPENBLAS_NUM_THREADS=1)"},
+                                   f"{args.config} stream after the 100-frame statistics window "
+                                   f"({'the reference package prost.jobs.StreamTracker.push' if kind == 'reference' else 'numpy port of the reference path'}, "
+                                   "OPENBLAS_NUM_THREADS=1)"},
         "e2e": {"value": rate, "unit": "stream-frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -428,39 +464,69 @@ def main():
     resident_counters = native.resident_counters() if native.query(nat.Q_RESIDENT) else None
     native.profile(False)
 
-    # end to end through the public API: pinned host frames in, host mask + bg out
+    # end to end through the public API (BatchTracker.push, the StreamTracker
+    # seam batched): pinned HOST frames in — 8-bit camera frames, divided by
+    # 255 on the device like frameio.py:136 — and, per stream-frame, the
+    # FrameRecord fields out (jobs.py:142-151): mask, raw_mask and the
+    # FitInfo (fit_cost, step, frame_index, status; delivered asynchronously),
+    # plus the background frame with --e2e-background.  Host copies inside the
+    # timed region, pipelined against the kernels on the handle's streams.
     e2e = None
     if not args.no_e2e:
+        from paper_1302_2073_b200.tracker import FitInfoBuffer
+
+        u8 = not args.e2e_f32 and not pixel
         if host is not None:
-            host_pinned = torch.from_numpy(host).pin_memory()
-            e2e0, HF = 0, host_pinned.shape[0]
+            src = torch.from_numpy(host)
+            e2e0, HF = 0, src.shape[0]
         else:
             # the e2e frames continue the streams: stage them in pinned host memory
             e2e0, HF = step, e2e_frames
-            host_pinned = torch.empty((HF,) + tuple(frames_dev.shape[1:]), dtype=frames_dev.dtype,
-                                      pin_memory=True)
-            host_pinned.copy_(frames_dev[e2e0:e2e0 + HF])
-
+            src = frames_dev[e2e0:e2e0 + HF]
+        if u8:
+            host_pinned = torch.empty(tuple(src.shape), dtype=torch.uint8, pin_memory=True)
+            host_pinned.copy_(torch.clamp(torch.round(src.float() * 255.0), 0, 255).to(torch.uint8))
+        else:
+            host_pinned = torch.empty(tuple(src.shape), dtype=src.dtype, pin_memory=True)
+            host_pinned.copy_(src)
+        want_bg = args.e2e_background or pixel or args.e2e_f32
         mask_h = torch.empty((S, P_loc), dtype=torch.uint8).pin_memory()
-        bg_h = torch.empty((S, n_loc), dtype=bg.dtype).pin_memory()
+        raw_h = torch.empty((S, P_loc), dtype=torch.uint8).pin_memory()
+        bg_h = torch.empty((S, n_loc), dtype=bg.dtype).pin_memory() if want_bg else None
+        fit_h = FitInfoBuffer(S)
+
+        def push_e2e(frame):
+            if pixel:
+                do_push(frame, bg_h, mask_h)
+            else:
+                bt.push(frame, background=bg_h, mask=mask_h, raw_mask=raw_h, fit_out=fit_h)
+
         for _ in range(2):
-            do_push(host_pinned[(step - e2e0) % HF], bg_h, mask_h)
+            push_e2e(host_pinned[(step - e2e0) % HF])
             step += 1
         torch.cuda.synchronize()
+        native.synchronize()
         barrier()
         e0.record()
         for _ in range(args.steps):
-            do_push(host_pinned[(step - e2e0) % HF], bg_h, mask_h)
+            push_e2e(host_pinned[(step - e2e0) % HF])
             step += 1
         native.join(torch.cuda.current_stream().cuda_stream)  # the last step's copies too
         e1.record()
         torch.cuda.synchronize()
         barrier()
         ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+        d2h = S * P_loc + (0 if pixel else S * P_loc + fit_h.nbytes) + (
+            S * n_loc * bg_h.element_size() if want_bg else 0)
         e2e = {"value": units * args.steps / (ms_e2e / 1000.0), "unit": "stream-frames/s",
                "h2d_bytes_per_step": S * n_loc * host_pinned.element_size(),
-               "d2h_bytes_per_step": S * P_loc + S * n_loc * bg_h.element_size(),
-               "ms_per_step": ms_e2e / args.steps}
+               "d2h_bytes_per_step": d2h,
+               "ms_per_step": ms_e2e / args.steps,
+               "frames": "u8 (frame/255 on the device)" if u8 else str(host_pinned.dtype),
+               "outputs": ("mask, raw_mask, FitInfo" if not pixel else "mask") +
+                          (", background" if want_bg else "")}
+        if not pixel:
+            e2e["fit_cost_finite"] = bool(np.all(np.isfinite(fit_h.fit_costs())))
     native.synchronize()
 
     # roofline of the frame update (per GPU)
@@ -490,14 +556,20 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            rate, cores, frames, wall = cpu_rate(args.config, tracker, args.cpu_frames)
-            cpu = {"value": rate, "unit": "stream-frames/s", "cores": cores, "kind": "port",
+            rate, cores, frames, wall, kind = cpu_rate(args.config, tracker, args.cpu_frames)
+            cpu = {"value": rate, "unit": "stream-frames/s", "cores": cores, "kind": kind,
                    "cpu": cpu_model(),
                    "sample": f"{cores} worker processes x {args.cpu_frames} frames of their own "
-                             f"{args.config} stream (numpy oracle of the reference path, "
+                             f"{args.config} stream after the 100-frame statistics window "
+                             f"({'prost.jobs.StreamTracker.push, the reference package' if kind == 'reference' else 'numpy port of the reference path'}, "
                              f"OPENBLAS_NUM_THREADS=1; {wall:.1f} s wall)"}
+            if kind == "reference" and args.cpu_port:
+                prate, _, _, pwall, _ = cpu_rate(args.config, tracker, args.cpu_frames, cores,
+                                                 kind="port")
+                cpu["port_value"] = prate
+                cpu["reference_over_port"] = rate / prate
         except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "stream-frames/s", "cores": None, "kind": "port",
+            cpu = {"value": None, "unit": "stream-frames/s", "cores": None, "kind": reference_kind(),
                    "sample": f"failed: {exc!r}"}
 
     if rank == 0:

@@ -103,6 +103,10 @@ typedef struct prost_outputs {
   int32_t on_device;      /* 1: the array pointers above are device pointers */
   void* fit_residual;     /* x - U y after the fit, before the geodesic (FitResult.residual,
                              fit.py:50-63); same dtype / placement as background */
+  int32_t fit_async;      /* 1: `fit` is filled asynchronously (stream-ordered, pinned host
+                             memory; valid after prost_join / prost_synchronize) instead of
+                             making the call synchronous; a rejected (non-finite) frame then
+                             shows as its stream's status instead of the return code */
 } prost_outputs;
 
 typedef struct prost_handle prost_handle;

@@ -31,6 +31,7 @@ from .params import (
 )
 from .tracker import (
     BatchTracker,
+    FitInfoBuffer,
     FitResult,
     NativeTracker,
     StreamTracker,
@@ -47,7 +48,7 @@ __all__ = [
     "CodecError", "ConfigError", "DeviceError", "DimensionError", "NonFiniteError",
     "ProstError", "SequenceError", "SnapshotError", "FrameBuffer", "FrameRecord",
     "SegmentationMask", "DEFAULT_I_INIT", "CgOptions", "LpConfig", "ProstParams", "RunConfig",
-    "smoothing_from_threshold", "step_size", "tau_from_init", "BatchTracker", "FitResult",
+    "smoothing_from_threshold", "step_size", "tau_from_init", "BatchTracker", "FitInfoBuffer", "FitResult",
     "NativeTracker", "StreamTracker", "SubspaceBasis", "TrackerState", "bootstrap",
     "process_frame", "random_orthonormal", "__version__",
 ]

@@ -72,6 +72,7 @@ class Outputs(ctypes.Structure):
         ("mask", ctypes.c_void_p), ("raw_mask", ctypes.c_void_p),
         ("fit", ctypes.POINTER(FitInfo)), ("dtype", ctypes.c_int32),
         ("on_device", ctypes.c_int32), ("fit_residual", ctypes.c_void_p),
+        ("fit_async", ctypes.c_int32),
     ]
 
 

@@ -119,6 +119,8 @@ struct prost_handle {
   void* io_bg[2] = {};
   void* io_res[2] = {};
   uint8_t* io_mask[2] = {};
+  uint8_t* io_raw[2] = {};   // raw labels written by the kernels (pipelined host I/O)
+  FitInfo* io_info[2] = {};  // per-slot FitInfo written by the kernels (fit_async)
   int io_slot = 0, io_last = 0;
   bool io_pending = false;
   // optional per-phase timing (prost_profile)
@@ -596,8 +598,15 @@ int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStr
     rc = download_dense(h, h->fresbuf, o.fit_residual, odt, o.on_device, h->S * h->C, st);
   if (!rc && o.mask && a.mask_out == h->maskbuf) rc = copy_labels(h, h->maskbuf, o.mask, o.on_device, st);
   if (!rc && o.raw_mask && a.raw_out == nullptr) rc = copy_labels(h, h->lab, o.raw_mask, o.on_device, st);
+  if (!rc && o.raw_mask && a.raw_out != nullptr && a.raw_out != o.raw_mask)
+    rc = copy_labels(h, a.raw_out, o.raw_mask, o.on_device, st);  // a pipelined slot's raw labels
   if (rc) return rc;
-  if (o.fit) {
+  if (o.fit && o.fit_async) {
+    // stream-ordered copy into the caller's (pinned) array; statuses are the
+    // caller's to check once the push is joined
+    CK(cudaMemcpyAsync(o.fit, a.info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+  }
+  if (o.fit && !o.fit_async) {
     CK(cudaMemcpyAsync(h->info_h, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     std::memcpy(o.fit, h->info_h, (size_t)h->S * sizeof(FitInfo));
@@ -614,7 +623,7 @@ int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStr
     // no readback requested: peek at the frame indices asynchronously and
     // keep launching the cold-start kernel until every stream is past frame 0
     // (a stream whose first frame was rejected stays cold, fit.py:86-87)
-    CK(cudaMemcpyAsync(h->info_peek, h->info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->info_peek, a.info, (size_t)h->S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(h->ev_peek, st));
     h->peek_pending = true;
   }
@@ -702,6 +711,8 @@ int push_pipelined(prost_handle* h, const void* frames, int32_t dtype, const pro
       if (e == cudaSuccess) h->io_bg[i] = dev_alloc(fbytes, &e);
       if (e == cudaSuccess) h->io_res[i] = dev_alloc(fbytes, &e);
       if (e == cudaSuccess) h->io_mask[i] = (uint8_t*)dev_alloc((size_t)h->S * h->Pp, &e);
+      if (e == cudaSuccess) h->io_raw[i] = (uint8_t*)dev_alloc((size_t)h->S * h->Pp, &e);
+      if (e == cudaSuccess) h->io_info[i] = (FitInfo*)dev_alloc((size_t)h->S * sizeof(FitInfo), &e);
       if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "I/O buffers: %s", cudaGetErrorString(e));
     }
   }
@@ -718,6 +729,10 @@ int push_pipelined(prost_handle* h, const void* frames, int32_t dtype, const pro
   prost_outputs o{};
   int rc = push_setup(h, frames, dtype, 0, out, h->s_in, &a, &o);
   if (rc) return rc;
+  // raw labels and FitInfo go to this slot's own buffers: the next frame's
+  // kernels overwrite the label state and the handle's FitInfo
+  if (o.raw_mask) a.raw_out = h->io_raw[sl];
+  if (o.fit) a.info = h->io_info[sl];
   CK(cudaEventRecord(h->ev_in[sl], h->s_in));
   CK(cudaStreamWaitEvent(h->s_comp, h->ev_in[sl], 0));
   CK(cudaStreamWaitEvent(h->s_comp, h->ev_out[sl], 0));
@@ -962,7 +977,7 @@ void prost_destroy(prost_handle* h) {
   if (h->s_in) {
     cudaDeviceSynchronize();
     void* own[] = {h->io_x[1], h->io_bg[0], h->io_bg[1], h->io_res[0], h->io_res[1], h->io_mask[0],
-                   h->io_mask[1]};
+                   h->io_mask[1], h->io_raw[0], h->io_raw[1], h->io_info[0], h->io_info[1]};
     for (void* b : own)
       if (b && b != h->x && b != h->bgbuf && b != h->resbuf && b != h->maskbuf) cudaFree(b);
     if (h->io_x[0] != h->x) cudaFree(h->io_x[0]);
@@ -1141,9 +1156,10 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   Args a;
   prost_outputs o{};
   const char* nopipe = getenv("PROST_NO_PIPE");
-  // (raw labels are copied from the label state itself, which the next frame's
-  // kernels overwrite: no pipelining when they are requested)
-  if (!on_device && out && !out->on_device && !out->fit && !out->raw_mask && !out->fit_residual && !h->prof &&
+  // (raw labels and an asynchronous FitInfo go through per-slot buffers; a
+  // synchronous FitInfo readback or the fit residual disable pipelining)
+  if (!on_device && out && !out->on_device && (!out->fit || out->fit_async) && !out->fit_residual &&
+      !h->prof &&
       !(nopipe && nopipe[0] == '1'))
     return push_pipelined(h, frames, dtype, out, st);
   if (h->io_pending) {  // order after the pipelined pushes before this one

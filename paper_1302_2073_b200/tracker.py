@@ -187,6 +187,26 @@ def _buffer(a, writable=False):
     return ctypes.c_void_p(a.ctypes.data), code, 0, a.size
 
 
+class FitInfoBuffer:
+    """Pinned host array of n `prost_fit_info` records for asynchronous
+    delivery (`push(..., fit_out=buf)`); read it after the push is joined."""
+
+    def __init__(self, n: int):
+        import torch
+
+        self.n = n
+        self._t = torch.empty(n * ctypes.sizeof(nat.FitInfo), dtype=torch.uint8).pin_memory()
+        self.ptr = self._t.data_ptr()
+        self.nbytes = n * ctypes.sizeof(nat.FitInfo)
+
+    def records(self):
+        arr = (nat.FitInfo * self.n).from_address(self.ptr)
+        return [arr[i] for i in range(self.n)]
+
+    def fit_costs(self) -> np.ndarray:
+        return np.array([r.fit_cost for r in self.records()])
+
+
 class NativeTracker:
     """Owns one C-ABI handle: n_streams trackers sharing a parameter set."""
 
@@ -275,13 +295,19 @@ class NativeTracker:
 
     # -- frames --------------------------------------------------------------
     def push(self, frames, background=None, residual=None, mask=None, raw_mask=None,
-             fit: bool = True, cuda_stream: int = 0, fit_residual=None):
+             fit: bool = True, cuda_stream: int = 0, fit_residual=None, fit_out=None):
         """Enqueue one frame per stream.  Outputs are numpy arrays or torch
         tensors (host or device) to fill.  With fit=True the call waits and
         returns the per-stream `prost_fit_info` array.  `fit_residual` receives
-        x - U y after the fit, before the geodesic step (FitResult.residual)."""
+        x - U y after the fit, before the geodesic step (FitResult.residual).
+        `fit_out` (a `FitInfoBuffer`) receives the per-stream FitInfo without
+        synchronizing: it is valid after `join` / `synchronize`, and host-I/O
+        pushes stay pipelined."""
         fp, fdt, fdev, out = self._frame_and_outputs(frames, background, residual, mask,
-                                                     raw_mask, fit, fit_residual)
+                                                     raw_mask, fit and fit_out is None, fit_residual)
+        if fit_out is not None:
+            out.fit = ctypes.cast(ctypes.c_void_p(fit_out.ptr), ctypes.POINTER(nat.FitInfo))
+            out.fit_async = 1
         rc = self._lib.prost_push(self._h, fp, fdt, fdev, ctypes.byref(out),
                                   ctypes.c_void_p(cuda_stream))
         self._check(rc, "push")
@@ -669,9 +695,10 @@ class BatchTracker:
                 self.native.set_core_state(s, cache[sd], np.zeros(self.params.k), None, 0, 0)
 
     def push(self, frames, background=None, residual=None, mask=None, raw_mask=None,
-             fit: bool = False, cuda_stream: int = 0):
+             fit: bool = False, cuda_stream: int = 0, fit_out=None):
         return self.native.push(frames, background=background, residual=residual, mask=mask,
-                                raw_mask=raw_mask, fit=fit, cuda_stream=cuda_stream)
+                                raw_mask=raw_mask, fit=fit, cuda_stream=cuda_stream,
+                                fit_out=fit_out)
 
     def background_frame(self, out, cuda_stream: int = 0) -> None:
         self.native.background(out, cuda_stream=cuda_stream)

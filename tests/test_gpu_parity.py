@@ -504,3 +504,47 @@ def test_ragged_shapes_against_oracle(precision, shape):
         assert rel <= 1e-10 and ang <= 1e-9
     else:
         assert worst <= 0.01 and rel <= 1e-4 and ang <= 1e-3
+
+
+@pytest.mark.gpu
+def test_pipelined_u8_frames_f64_outputs_async_fit():
+    """Pinned 8-bit host frames in, float64 host backgrounds (converted through
+    the download staging buffer), masks, raw masks and an asynchronously
+    delivered FitInfo out, back to back on the pipelined path: identical to
+    the synchronous device-buffer path (upload and download staging are
+    separate buffers; raw labels and FitInfo have per-slot buffers)."""
+    import torch
+
+    W, H, S, F = 64, 48, 4, 9
+    cfg = pkg.RunConfig(subspace_dim=8, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=4, seed=0)
+    data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1)
+    q = np.clip(np.rint(data * 255.0), 0, 255).astype(np.uint8)
+    dev_bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    host_bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    mask_d = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+    raw_d = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+    bg_d = torch.empty((S, W * H), dtype=torch.float64, device="cuda")
+    ref = []
+    for f in range(F):
+        info = dev_bt.push(torch.from_numpy(q[f]).cuda(), background=bg_d, mask=mask_d,
+                           raw_mask=raw_d, fit=True)
+        ref.append((mask_d.cpu().numpy(), raw_d.cpu().numpy(), bg_d.cpu().numpy(),
+                    [info[s].fit_cost for s in range(S)], [info[s].frame_index for s in range(S)]))
+    frames_h = [torch.from_numpy(q[f]).pin_memory() for f in range(F)]
+    outs = [(torch.empty((S, W * H), dtype=torch.uint8).pin_memory(),
+             torch.empty((S, W * H), dtype=torch.uint8).pin_memory(),
+             torch.empty((S, W * H), dtype=torch.float64).pin_memory(),
+             pkg.FitInfoBuffer(S)) for _ in range(F)]
+    for f in range(F):
+        m, r, b, fi = outs[f]
+        host_bt.push(frames_h[f], background=b, mask=m, raw_mask=r, fit_out=fi)
+    host_bt.join()
+    torch.cuda.synchronize()
+    for f in range(F):
+        m, r, b, fi = outs[f]
+        np.testing.assert_array_equal(m.numpy(), ref[f][0])
+        np.testing.assert_array_equal(r.numpy(), ref[f][1])
+        np.testing.assert_array_equal(b.numpy(), ref[f][2])
+        np.testing.assert_array_equal(fi.fit_costs(), np.array(ref[f][3]))
+        assert [rec.frame_index for rec in fi.records()] == ref[f][4]

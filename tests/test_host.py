@@ -36,7 +36,7 @@ def test_struct_layouts_match_header():
 
     assert ctypes.sizeof(_native.Params) == 8 * 4 + 11 * 8
     assert ctypes.sizeof(_native.FitInfo) == 8 * 3 + 4 * 4
-    assert ctypes.sizeof(_native.Outputs) == 5 * 8 + 2 * 4 + 8  # + fit_residual (ABI 2)
+    assert ctypes.sizeof(_native.Outputs) == 5 * 8 + 2 * 4 + 8 + 8  # + fit_residual, fit_async (ABI 2)
 
 
 def test_create_validates_before_touching_the_device():
