@@ -1483,7 +1483,7 @@ int prost_resident_counters(prost_handle* h, int64_t* out, int32_t n) {
   // converted from SM clocks to ns with the CTA's own clock rate), then the
   // max kernel time
   const bool is_time[PROF_N] = {true, true, true, true, true, false, false,
-                                true, true, true, true, false, true, true};
+                                true, true, true, true, false, true, true, true};
   std::vector<double> acc(PROF_N, 0.0);
   unsigned long long mx = 0;
   for (int c = 0; c < ctas; ++c) {

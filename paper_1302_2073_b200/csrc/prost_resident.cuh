@@ -43,6 +43,7 @@ enum {
   PROF_GT_TOTAL,  // kernel time in %globaltimer ns (the others count SM clocks)
   PROF_SW_OWN,    // k_tmem CG iteration sweeps: thread 0's own sweep + staging
   PROF_SW_ALL,    //   ... until every warp of the CTA has staged its partials
+  PROF_LOGIC_ITER,  // k_tmem: scalar logic after the CG iteration sweeps only
   PROF_N = 16
 };
 

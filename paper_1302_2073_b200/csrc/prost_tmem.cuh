@@ -812,7 +812,11 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
         }
         team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
-        LOGIC(TM_AFTER_ITER<K>(cs, a, s, lt, red, wlo));
+        {
+          const unsigned long long tli = (ra.prof && tid == 0) ? ptimer() : 0;
+          LOGIC(TM_AFTER_ITER<K>(cs, a, s, lt, red, wlo));
+          if (ra.prof && tid == 0) sprof[PROF_LOGIC_ITER] += ptimer() - tli;
+        }
       }
       group_sync<NG>(g);
     }

@@ -428,7 +428,8 @@ class NativeTracker:
         d = {nm: out[i] / 1e3 for i, nm in enumerate(names)}
         d.update(team_sums=int(out[5]), rounds=int(out[6]), slowest_kernel_us=out[n - 1] / 1e3)
         for i, nm in ((7, "phase_stats_us"), (8, "phase_pass0_us"), (9, "phase_iter_us"),
-                      (10, "phase_geo_us"), (12, "iter_sweep_own_us"), (13, "iter_sweep_all_us")):
+                      (10, "phase_geo_us"), (12, "iter_sweep_own_us"), (13, "iter_sweep_all_us"),
+                      (14, "logic_iter_us")):
             d[nm] = out[i] / 1e3
         return d
 
