@@ -435,6 +435,7 @@ def main():
     clocks.start()
     time.sleep(0.3)
     launches0 = native.launches
+    ex0 = st.exchanges if pixel else 0
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -448,6 +449,7 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1)
     launches = native.launches - launches0
+    ex_timed = (st.exchanges - ex0) / args.steps if pixel else None
     clk = clocks.stop()
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps
@@ -598,6 +600,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gen_seconds": t_gen,
+            "exchanges_per_frame": ex_timed,
             "preroll": {"frames": preroll, "seconds": t_pre,
                         "note": "untimed frames through the i_init statistics window before warm-up; "
                                 "the timed steps are steady-state frames (90% of a 1000-frame run)"},

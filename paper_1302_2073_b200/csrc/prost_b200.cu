@@ -94,6 +94,9 @@ struct prost_handle {
   size_t stage_bytes[2] = {0, 0};
   long long launches = 0;
   bool maybe_cold = true;
+  // every stream is known (from a FitInfo readback or peek) to be past its
+  // statistics window: the exchange program drops the statistics phase
+  bool stats_over = false;
   // upper bound on every stream's steps-since-QR before the next push: the
   // periodic re-orthonormalization kernels are launched only when it can be due
   long long qr_bound = 0;
@@ -470,9 +473,13 @@ int copy_labels(prost_handle* h, const uint8_t* src, uint8_t* dst, int on_device
 // Retire a finished non-blocking FitInfo peek (see push_outputs).
 void retire_peek(prost_handle* h) {
   if (!h->peek_pending || cudaEventQuery(h->ev_peek) != cudaSuccess) return;
-  bool cold = false;
-  for (int s = 0; s < h->S; ++s) cold |= h->info_peek[s].frame_index == 0;
+  bool cold = false, over = true;
+  for (int s = 0; s < h->S; ++s) {
+    cold |= h->info_peek[s].frame_index == 0;
+    over &= h->info_peek[s].frame_index > h->prm.i_init;  // frozen (pipeline.py:142-146)
+  }
   h->maybe_cold = cold;
+  h->stats_over = h->stats_over || over;
   h->peek_pending = false;
 }
 
@@ -611,15 +618,17 @@ int push_outputs(prost_handle* h, const Args& a, const prost_outputs& o, cudaStr
     CK(cudaStreamSynchronize(st));
     std::memcpy(o.fit, h->info_h, (size_t)h->S * sizeof(FitInfo));
     int first_bad = PROST_OK;
-    bool cold = false;
+    bool cold = false, over = true;
     for (int s = 0; s < h->S; ++s) {
       if (h->info_h[s].status != PROST_OK && first_bad == PROST_OK) first_bad = h->info_h[s].status;
       cold |= h->info_h[s].frame_index == 0;  // rejected at its first frame: still cold
+      over &= h->info_h[s].frame_index > h->prm.i_init;
     }
     h->maybe_cold = cold;
+    h->stats_over = h->stats_over || over;
     h->peek_pending = false;
     if (first_bad != PROST_OK) return fail(h, first_bad, "frame contains non-finite values");
-  } else if (h->maybe_cold && !h->peek_pending) {
+  } else if ((h->maybe_cold || (h->xmode && h->pipeline && !h->stats_over)) && !h->peek_pending) {
     // no readback requested: peek at the frame indices asynchronously and
     // keep launching the cold-start kernel until every stream is past frame 0
     // (a stream whose first frame was rejected stays cold, fit.py:86-87)
@@ -1051,8 +1060,9 @@ int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const
   CK(cudaMemcpy(h->ctl + stream, &c, sizeof c, cudaMemcpyHostToDevice));
   if (frame_index == 0) {
     h->maybe_cold = true;
-    h->peek_pending = false;  // an older peek predates this state
   }
+  h->stats_over = false;
+  h->peek_pending = false;  // an older peek predates this state
   return PROST_OK;
 }
 
@@ -1117,6 +1127,8 @@ int prost_set_preproc(prost_handle* h, int32_t stream, const double* mean, const
     c.frozen = sc[4] != 0.0;
     c.pstd = sc[5];
     CK(cudaMemcpy(h->ctl + stream, &c, sizeof c, cudaMemcpyHostToDevice));
+    h->stats_over = false;
+    h->peek_pending = false;
   }
   return PROST_OK;
 }
@@ -1217,7 +1229,15 @@ int prost_xbegin(prost_handle* h, const void* frames, int32_t dtype, int32_t on_
   if (rc) return rc;
   std::vector<int>& pg = h->xprog;
   pg.clear();
-  if (h->pipeline) pg.push_back(XS_STATS);
+  // The statistics phase is a no-op once every stream is frozen, but its
+  // exchange is not: drop it once a FitInfo peek has shown every stream past
+  // the window.  While that is open the peek is retired synchronously, so all
+  // ranks (same stream, same frame indices) build the same program.
+  if (h->pipeline && !h->stats_over && h->peek_pending) {
+    CK(cudaEventSynchronize(h->ev_peek));
+    retire_peek(h);
+  }
+  if (h->pipeline && !h->stats_over) pg.push_back(XS_STATS);
   if (h->maybe_cold) pg.push_back(XS_COLD);
   pg.push_back(XS_PASS0);
   for (int it = 0; it < h->prm.cg_max_iters; ++it) {

@@ -94,7 +94,8 @@ class ShardedTracker:
         self.xred = torch.as_tensor(_CudaArray(ptr, cnt, "<f8"), device=f"cuda:{device}")
         self.edges = torch.zeros((2, W), dtype=torch.uint8, device=f"cuda:{device}")
         self.gathered = torch.zeros((self.world, 2, W), dtype=torch.uint8, device=f"cuda:{device}")
-        self.exchanges = 0
+        self.exchanges = 0  # cross-rank all-reduces issued (the exchange program)
+        self.frames = 0
 
     # -- layout ---------------------------------------------------------------
     def local_rows(self, full):
@@ -148,6 +149,7 @@ class ShardedTracker:
         nt = self.native
         nt.xbegin(block, background=background, residual=residual, mask=mask, raw_mask=raw_mask,
                   fit=fit, cuda_stream=cuda_stream)
+        self.frames += 1
         while nt.xnext(cuda_stream):
             with self._on(cuda_stream):
                 self._allreduce(self.xred)

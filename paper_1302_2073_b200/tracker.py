@@ -529,17 +529,25 @@ class StreamTracker:
     def frame_index(self) -> int:
         return self._frame_index
 
-    def _prepare(self, frame: FrameBuffer) -> FrameBuffer:
-        # jobs.py:181-184: gray conversion, then bilinear resampling to the
-        # model resolution (on the device, resample.py; identity sizes pass)
+    def _prepare(self, frame: FrameBuffer):
+        """jobs.py:181-184: gray conversion, then bilinear resampling to the
+        model resolution.  Returns (channels, data): an off-resolution frame
+        is resampled on the device (resample.py, fp64 like the reference) and
+        stays there — the push reads the device tensor, with no round trip
+        through the host; identity sizes pass the host data through."""
         if self.config.grayscale:
             frame = frame.to_gray()
         if (frame.width, frame.height) != (self.config.target_width, self.config.target_height):
-            from .resample import resample
+            import torch
 
-            frame = resample(frame, self.config.target_width, self.config.target_height,
-                             device=self.device)
-        return frame
+            from .resample import resample_device
+
+            src = torch.from_numpy(np.ascontiguousarray(frame.data)).to(f"cuda:{self.device}")
+            out = resample_device(src, frame.channels, frame.width, frame.height,
+                                  self.config.target_width, self.config.target_height,
+                                  out_dtype=torch.float64)
+            return frame.channels, out
+        return frame.channels, frame.data
 
     def _start(self, channels: int) -> None:
         w, hgt = self.config.target_width, self.config.target_height
@@ -553,21 +561,21 @@ class StreamTracker:
 
     def push(self, frame: FrameBuffer) -> FrameRecord:
         """Run the full pipeline on one frame and advance the model (jobs.py:186-229)."""
-        prepared = self._prepare(frame)
+        channels, data = self._prepare(frame)
         if self._native is None:
-            self._start(prepared.channels)
-        elif prepared.channels != self.channels:
-            raise SequenceError(f"frame has {prepared.channels} channels, expected {self.channels}")
+            self._start(channels)
+        elif channels != self.channels:
+            raise SequenceError(f"frame has {channels} channels, expected {self.channels}")
         n = self._native
         t = step_size(self._frame_index, self.params)
         mask = np.empty(n.pixels, dtype=np.uint8)
         raw = np.empty(n.pixels, dtype=np.uint8)
         residual = np.empty(n.m)
-        data = prepared.data
-        if data.dtype not in (np.float64, np.float32, np.uint8):
-            data = data.astype(np.float64)
-        info = n.push(np.ascontiguousarray(data), residual=residual, mask=mask, raw_mask=raw,
-                      fit=True)[0]
+        if isinstance(data, np.ndarray):
+            if data.dtype not in (np.float64, np.float32, np.uint8):
+                data = data.astype(np.float64)
+            data = np.ascontiguousarray(data)
+        info = n.push(data, residual=residual, mask=mask, raw_mask=raw, fit=True)[0]
         self._frame_index = int(info.frame_index)
         w, hgt = self.config.target_width, self.config.target_height
         return FrameRecord(

@@ -548,3 +548,23 @@ def test_pipelined_u8_frames_f64_outputs_async_fit():
         np.testing.assert_array_equal(b.numpy(), ref[f][2])
         np.testing.assert_array_equal(fi.fit_costs(), np.array(ref[f][3]))
         assert [rec.frame_index for rec in fi.records()] == ref[f][4]
+
+
+@pytest.mark.gpu
+def test_off_resolution_frames_stay_on_device():
+    """Off-resolution frames are resampled on the device and pushed from there
+    (jobs.py:181-184): the same records as pushing the host-resampled frames
+    (pipeline.py:164-193, bit-identical fp64 resampling)."""
+    from paper_1302_2073_b200.resample import resample
+
+    rng = np.random.default_rng(4)
+    cfg = pkg.RunConfig(subspace_dim=4, p=0.5, mu=1e-4, cg_max_iters=2, target_width=24,
+                        target_height=16, grayscale=True, i_init=3, seed=1)
+    a, b = pkg.StreamTracker(cfg), pkg.StreamTracker(cfg)
+    for _ in range(6):
+        fb = pkg.FrameBuffer(37, 21, 1, rng.random(37 * 21))
+        ra = a.push(fb)
+        rb = b.push(resample(fb, 24, 16))
+        np.testing.assert_array_equal(ra.mask.labels, rb.mask.labels)
+        np.testing.assert_array_equal(ra.residual, rb.residual)
+        assert ra.fit_cost == rb.fit_cost
