@@ -139,6 +139,17 @@ int prost_get_preproc(prost_handle* h, int32_t stream, double* mean, double* sca
 int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
                const prost_outputs* out, void* cuda_stream);
 
+/* F consecutive frames of every stream in one call (frame blocking: each
+ * stream's slice stays on chip across its F frames, U crosses HBM once per
+ * block).  frames [F][n_streams][n]; outputs [F][n_streams][...] (masks
+ * unpadded, [F][n_streams][width*height]); out->fit [F][n_streams].  Results
+ * equal F calls of prost_push.  Blocks on the TMEM kernel for fp32,
+ * one-channel, width*height % 4 == 0, fp32 outputs; otherwise it runs F
+ * single-frame pushes.  (No reference counterpart: StreamTracker.push
+ * called F times, jobs.py:186-229.) */
+int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_t dtype,
+                    int32_t on_device, const prost_outputs* out, void* cuda_stream);
+
 /* background_frame() for every stream into out [n_streams][n] (pipeline mode). */
 int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_device,
                      void* cuda_stream);

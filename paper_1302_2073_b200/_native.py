@@ -26,6 +26,7 @@ Q_RESIDENT, Q_TEAM, Q_TEAMS, Q_GROUPS, Q_QPC = 5, 6, 7, 8, 9
 EXPORTS = (
     "prost_abi_version", "prost_create", "prost_destroy", "prost_set_core_state",
     "prost_get_core_state", "prost_set_preproc", "prost_get_preproc", "prost_push",
+    "prost_push_many",
     "prost_background", "prost_synchronize", "prost_last_error", "prost_query",
     "prost_set_wave", "prost_profile", "prost_profile_read", "prost_resident_counters",
     "prost_set_exchange", "prost_xbuffer", "prost_xbegin", "prost_xnext", "prost_xapply",
@@ -100,6 +101,7 @@ def lib() -> ctypes.CDLL:
     L.prost_set_preproc.argtypes = [vp, i32, dp, dp]
     L.prost_get_preproc.argtypes = [vp, i32, dp, dp]
     L.prost_push.argtypes = [vp, vp, i32, i32, ctypes.POINTER(Outputs), vp]
+    L.prost_push_many.argtypes = [vp, vp, i32, i32, i32, ctypes.POINTER(Outputs), vp]
     L.prost_background.argtypes = [vp, vp, i32, i32, vp]
     L.prost_synchronize.argtypes = [vp]
     L.prost_last_error.argtypes = [vp, ctypes.c_char_p, i32]

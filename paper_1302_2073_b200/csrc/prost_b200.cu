@@ -86,6 +86,16 @@ struct prost_handle {
   void* bgbuf = nullptr;
   void* resbuf = nullptr;
   void* fresbuf = nullptr;  // fit residual (FitResult.residual) when it cannot be written in place
+  // frame-blocked pushes (prost_push_many): [F][S][...] staging
+  void* xblk = nullptr;
+  size_t xblk_bytes = 0;
+  void* oblk[3] = {nullptr, nullptr, nullptr};  // background, residual, fit residual
+  size_t oblk_bytes = 0;
+  uint8_t* rawblk = nullptr;
+  uint8_t* maskblk = nullptr;
+  size_t lblk_bytes = 0;
+  FitInfo* infoblk = nullptr;
+  int infoblk_n = 0;
   uint8_t* maskbuf = nullptr;
   // conversion staging: uploads (frames) and downloads (outputs) have their
   // own buffers, so a pipelined push's upload of frame N+1 on s_in never
@@ -978,6 +988,7 @@ void prost_destroy(prost_handle* h) {
   if (!h) return;
   void* bufs[] = {h->U, h->r, h->ud, h->x, h->mean, h->lab, h->ctl, h->part, h->cnt,
                   h->rinv, h->info, h->bgbuf, h->resbuf, h->fresbuf, h->maskbuf, h->stage[0], h->stage[1],
+                  h->xblk, h->oblk[0], h->oblk[1], h->oblk[2], h->rawblk, h->maskblk, h->infoblk,
                   h->rbar, h->rpart, h->rprof, h->xred, h->xgo, h->labc};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1157,6 +1168,158 @@ int prost_get_preproc(prost_handle* h, int32_t stream, double* mean, double* sc)
     sc[4] = c.frozen ? 1.0 : 0.0;
     sc[5] = c.pstd;
   }
+  return PROST_OK;
+}
+
+// Grow-only device scratch for frame-blocked pushes.
+int grow(prost_handle* h, void** p, size_t* have, size_t need) {
+  if (*have >= need && *p) return PROST_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e != cudaSuccess) return fail(h, PROST_ERR_CUDA, "block buffer: %s", cudaGetErrorString(e));
+  *have = need;
+  return PROST_OK;
+}
+
+int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
+               const prost_outputs* out, void* cuda_stream);
+
+// F consecutive frames of every stream in one launch (frame blocking, see
+// prost_tmem.cuh): frames [F][S][C*P], outputs [F][S][...], fit [F][S].
+// Where the TMEM kernel cannot block (fp64, 3 channels, padded planes, the
+// periodic QR possibly inside the block) it runs F single-frame pushes.
+int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_t dtype,
+                    int32_t on_device, const prost_outputs* out, void* cuda_stream) {
+  if (!h) return PROST_ERR_CONFIG;
+  if (nframes < 1) return fail(h, PROST_ERR_DIMENSION, "nframes must be >= 1, got %d", nframes);
+  if (h->xmode) return fail(h, PROST_ERR_CONFIG, "exchange-mode handle: use prost_xbegin");
+  if (dtype != PROST_F32 && dtype != PROST_F64 && dtype != PROST_U8)
+    return fail(h, PROST_ERR_CONFIG, "unknown frame dtype %d", dtype);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  prost_outputs o{};
+  if (out) o = *out;
+  const int S = h->S, P = h->P;
+  const size_t n = (size_t)h->C * P;
+  const size_t fsz = dtype_size(dtype);
+  const int odt = o.dtype == PROST_F64 ? PROST_F64 : PROST_F32;
+  const size_t osz = dtype_size(odt);
+  const bool dense = h->P == h->Pp;
+  const bool blockable = nframes > 1 && h->tmem && h->C == 1 && dense && dtype != PROST_F64 &&
+                         odt == PROST_F32 && h->qr_bound + nframes < QR_EVERY - 1;
+  if (!blockable) {
+    for (int f = 0; f < nframes; ++f) {
+      prost_outputs of = o;
+      auto at = [&](void* base, size_t per) { return base ? (void*)((char*)base + (size_t)f * S * per) : nullptr; };
+      of.background = at(o.background, n * osz);
+      of.residual = at(o.residual, n * osz);
+      of.fit_residual = at(o.fit_residual, n * osz);
+      of.mask = (uint8_t*)at(o.mask, P);
+      of.raw_mask = (uint8_t*)at(o.raw_mask, P);
+      of.fit = o.fit ? o.fit + (size_t)f * S : nullptr;
+      const int rc = prost_push(h, (const char*)frames + (size_t)f * S * n * fsz, dtype, on_device, &of, st);
+      if (rc) return rc;
+    }
+    return PROST_OK;
+  }
+  CK(cudaSetDevice(h->device));
+  {
+    int drc = io_drain(h);  // order after pipelined single-frame pushes
+    if (drc) return drc;
+  }
+  retire_peek(h);
+  h->qr_due = false;
+  h->qr_bound += nframes;
+  // frames: used in place on the device, else uploaded as they are (u8 stays u8)
+  const void* xdev = frames;
+  if (!on_device) {
+    const size_t bytes = (size_t)nframes * S * n * fsz;
+    int rc = grow(h, &h->xblk, &h->xblk_bytes, bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->xblk, frames, bytes, cudaMemcpyHostToDevice, st));
+    xdev = h->xblk;
+  }
+  Args a = make_args(h, 0);
+  a.x = xdev;
+  a.xu8 = dtype == PROST_U8 ? 1 : 0;
+  a.nframes = nframes;
+  const size_t obytes = (size_t)nframes * S * n * 4;
+  void* ouser[3] = {o.background, o.residual, o.fit_residual};
+  void** oarg[3] = {&a.bg_out, &a.res_out, &a.fitres_out};
+  for (int i = 0; i < 3; ++i) {
+    if (!ouser[i]) continue;
+    if (o.on_device) {
+      *oarg[i] = ouser[i];
+    } else {
+      if (h->oblk_bytes < obytes) {
+        for (int j = 0; j < 3; ++j) {
+          if (h->oblk[j]) cudaFree(h->oblk[j]);
+          h->oblk[j] = nullptr;
+        }
+        h->oblk_bytes = obytes;
+      }
+      if (!h->oblk[i]) CK(cudaMalloc(&h->oblk[i], h->oblk_bytes));
+      *oarg[i] = h->oblk[i];
+    }
+  }
+  // raw labels of every frame (the median reads them); the filtered masks
+  const size_t lbytes = (size_t)nframes * S * h->Pp;
+  if (o.mask || o.raw_mask) {
+    if (h->lblk_bytes < lbytes) {
+      if (h->rawblk) cudaFree(h->rawblk);
+      if (h->maskblk) cudaFree(h->maskblk);
+      h->rawblk = h->maskblk = nullptr;
+      h->lblk_bytes = lbytes;
+    }
+    if (!h->rawblk) CK(cudaMalloc(&h->rawblk, h->lblk_bytes));
+    if (!h->maskblk) CK(cudaMalloc(&h->maskblk, h->lblk_bytes));
+    a.raw_out = (o.raw_mask && o.on_device) ? o.raw_mask : h->rawblk;
+  }
+  if (h->infoblk_n < nframes * S) {
+    if (h->infoblk) cudaFree(h->infoblk);
+    h->infoblk = nullptr;
+    CK(cudaMalloc(&h->infoblk, (size_t)nframes * S * sizeof(FitInfo)));
+    h->infoblk_n = nframes * S;
+  }
+  a.info = h->infoblk;
+  const char* stg = getenv("PROST_STAGGER_NS");
+  RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
+           h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, 0, 1};
+  CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
+  {
+    PhaseTimer pt_(h, st, PROST_PH_FRAME);
+    CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng).launch(a, ra, h->rsmem, st));
+  }
+  h->launches += 1;
+  if (o.mask) {
+    PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
+    for (int f = 0; f < nframes; ++f) {
+      Args am = a;
+      am.lab = a.raw_out + (size_t)f * S * h->Pp;
+      am.mask_out = (o.on_device ? o.mask : h->maskblk) + (size_t)f * S * h->Pp;
+      launch_median(h, am, st, S);
+      h->launches += 1;
+    }
+  }
+  CK(cudaGetLastError());
+  // host outputs
+  if (!o.on_device) {
+    for (int i = 0; i < 3; ++i)
+      if (ouser[i]) CK(cudaMemcpyAsync(ouser[i], *oarg[i], obytes, cudaMemcpyDeviceToHost, st));
+    if (o.mask) CK(cudaMemcpyAsync(o.mask, h->maskblk, lbytes, cudaMemcpyDeviceToHost, st));
+    if (o.raw_mask) CK(cudaMemcpyAsync(o.raw_mask, h->rawblk, lbytes, cudaMemcpyDeviceToHost, st));
+  }
+  if (o.fit) {
+    CK(cudaMemcpyAsync(o.fit, h->infoblk, (size_t)nframes * S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+    if (!o.fit_async) {
+      CK(cudaStreamSynchronize(st));
+      for (int i = 0; i < nframes * S; ++i)
+        if (o.fit[i].status != PROST_OK) return fail(h, o.fit[i].status, "frame contains non-finite values");
+    }
+  }
+  h->maybe_cold = false;  // every stream ran its first frame at f = 0 (a rejected one stays at 0)
+  if (o.fit && !o.fit_async)
+    for (int i = 0; i < S; ++i) h->maybe_cold |= o.fit[(size_t)(nframes - 1) * S + i].frame_index == 0;
   return PROST_OK;
 }
 

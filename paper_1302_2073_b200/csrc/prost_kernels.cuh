@@ -74,6 +74,7 @@ struct Ctl {
   int it, active, need_lsfb, need_gradfb, acc_idx, ls_next, gwin_lo, last_acc;
   int do_geo, qr_now, status, iterations, cost_evals, grad_evals, frozen, cold;
   int update_stats, no_info;  // no_info: this copy must not write FitInfo
+  int info_slot;              // FitInfo row of this frame (frame-blocked pushes: f * S)
 };
 
 struct FitInfo {  // layout-identical to prost_fit_info
@@ -110,6 +111,8 @@ struct Args {
   const uint8_t* halo_bot;  // [S][width] label row below the local rows, or null
   uint8_t* labc;       // [S][np] per-coordinate flags of the TMEM kernel (3 channels), or null
   int xu8;             // TMEM kernel: x holds 8-bit frames, divided by 255 on load (frameio.py:136)
+  int nframes;         // TMEM kernel: consecutive frames per stream in this launch (frame blocking;
+                       // x, outputs and info are [nframes][S][...]); 0 or 1: one frame
   int s0;              // first stream of this launch
   int k, C, P, Pp, width, height;
   long long np;        // padded coordinates per stream = C * Pp
@@ -361,7 +364,7 @@ __device__ PROST_LOGIC void write_info(Ctl* c, const Args& a, int s) {
   fi.cost_evals = c->cost_evals;
   fi.grad_evals = c->grad_evals;
   fi.status = c->status;
-  a.info[s] = fi;
+  a.info[s + c->info_slot] = fi;
 }
 
 // End of the CG loop: projected-gradient norm, geodesic scalars

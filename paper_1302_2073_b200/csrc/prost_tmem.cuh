@@ -236,10 +236,23 @@ struct TmemRows {
     tmem_ld_row<RS>(taddr + e * RS, u);
     tmem_wait_ld();
   }
+  // write a row group back (frame blocking): K values per row, the weight
+  // in column RS-1 when k < RS (pair with tmem_wait_st before the next read)
+  template <int K>
+  __device__ __forceinline__ void store(const float (&up)[4][K], const float (&wn)[4]) const {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float row[RS];
+#pragma unroll
+      for (int j = 0; j < RS; ++j) row[j] = j < K ? up[e][j] : 0.f;
+      if (K < RS) row[RS - 1] = wn[e];
+      tmem_st_row<RS>(taddr + e * RS, row);
+    }
+  }
 };
 template <int RS>
 struct SmemRows {
-  const float4* base;  // row e, column group g at base[(e * RS/4 + g) * qs]
+  float4* base;  // row e, column group g at base[(e * RS/4 + g) * qs]
   int qs;
   bool ok;
   __device__ __forceinline__ void operator()(int e, float (&u)[RS]) const {
@@ -247,6 +260,21 @@ struct SmemRows {
     for (int g4 = 0; g4 < RS / 4; ++g4) {
       const float4 t = ok ? base[(size_t)(e * (RS / 4) + g4) * qs] : make_float4(0.f, 0.f, 0.f, 0.f);
       u[4 * g4] = t.x; u[4 * g4 + 1] = t.y; u[4 * g4 + 2] = t.z; u[4 * g4 + 3] = t.w;
+    }
+  }
+  template <int K>
+  __device__ __forceinline__ void store(const float (&up)[4][K], const float (&wn)[4]) const {
+    if (!ok) return;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float row[RS];
+#pragma unroll
+      for (int j = 0; j < RS; ++j) row[j] = j < K ? up[e][j] : 0.f;
+      if (K < RS) row[RS - 1] = wn[e];
+#pragma unroll
+      for (int g4 = 0; g4 < RS / 4; ++g4)
+        base[(size_t)(e * (RS / 4) + g4) * qs] =
+            make_float4(row[4 * g4], row[4 * g4 + 1], row[4 * g4 + 2], row[4 * g4 + 3]);
     }
   }
 };
@@ -420,6 +448,34 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     SYNC_FLOATS();
     group_sync<NG>(g);
 
+    // Frame blocking (a.nframes = F > 1, one channel): the stream's next F
+    // frames run while its slice stays on chip — U is loaded once and stored
+    // once per block, each frame's geodesic sweep writes U' back to TMEM /
+    // shared memory and runs the next frame's pass 0 on the rows it just
+    // updated (r0 = x_{f+1} - U'y_f: the warm start is this frame's y), and
+    // the per-frame outputs go to [f][S][...].  Every frame computes exactly
+    // what one push per frame computes.
+    const int F = (a.nframes > 1 && a.C == 1) ? a.nframes : 1;
+    bool p0_ready = false;  // this frame's pass 0 partials came with the last geodesic sweep
+    double cost_n = 0.0;
+    bool bad_n = false;
+    float pk_n[K + 1];
+#pragma unroll
+    for (int j = 0; j <= K; ++j) pk_n[j] = 0.f;
+    for (int f = 0; f < F; ++f) {
+    const size_t fo = (size_t)f * ra.S * a.np;  // this frame's coordinate outputs / input
+    const size_t fl = (size_t)f * ra.S * a.Pp;  // this frame's label outputs
+    const size_t sox = fo + so;                 // this frame's input of this stream
+    if (f > 0) {
+      if (lt == 0) {
+        cs->t = step_size(a, cs->frame_index);
+        cs->info_slot = f * ra.S;
+      }
+      group_sync<NG>(g);
+    } else if (lt == 0) {
+      cs->info_slot = 0;
+    }
+
     unsigned long long tph = (ra.prof && tid == 0) ? ptimer() : 0;
 #define PHASE_MARK(idx)                              \
   do {                                               \
@@ -439,7 +495,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         if (qi >= qcount) continue;
         const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float xv[4];
-        ld_x4(so + coord, xv);
+        ld_x4(sox + coord, xv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (pix + e < a.P) {
@@ -493,7 +549,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       const bool ok = qi < qcount;
       const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
       float xv[4] = {0.f, 0.f, 0.f, 0.f};
-      if (ok) ld_x4(so + coord, xv);
+      if (ok) ld_x4(sox + coord, xv);
       if (a.pipeline) {
         float mv[4];
         f4(ok ? *reinterpret_cast<const float4*>(Mg + so + coord) : z4, mv);
@@ -530,13 +586,15 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     const bool frame_ok = cs->status == ST_OK;
     const bool cold = frame_ok && cs->frame_index == 0;
     const bool fuse = frame_ok && !cold;
-    bool bad = false;
+    const bool use_p0 = f > 0 && p0_ready && frame_ok && !upd;
+    bool bad = use_p0 ? bad_n : false;
     bool mean_pending = upd;  // running-mean update not yet written this frame
-    double cost = 0.0;
+    double cost = use_p0 ? cost_n : 0.0;
     float pk[K + 1];
 #pragma unroll
-    for (int j = 0; j <= K; ++j) pk[j] = 0.f;
-    if (frame_ok) {
+    for (int j = 0; j <= K; ++j) pk[j] = use_p0 ? pk_n[j] : 0.f;
+    p0_ready = false;
+    if (frame_ok && f == 0) {
       const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
       const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
       for (int slot = 0; slot < nslots; ++slot) {
@@ -598,10 +656,13 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 
     if (frame_ok) {
       // ---- cold start y = U^T x (fit.py:86-87), then pass 0 over the slice ---
-      if (cold) {
+      // (also: a blocked frame whose pass 0 did not come with the geodesic
+      // sweep — statistics window, or the previous frame was rejected)
+      if (cold || (f > 0 && !use_p0)) {
         float pkc[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) pkc[j] = 0.f;
+        if (cold) {
         sweep([&](int qi, const auto& rows) {
           float xh[4];
           xhat(qi, upd, xh, bad);
@@ -624,6 +685,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           SYNC_FLOATS();
         }
         group_sync<NG>(g);
+        }
         if (cs->status == ST_OK) {
           sweep([&](int qi, const auto& rows) {
             float xh[4], w[4], r[4];
@@ -839,12 +901,26 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       // recurrence of accepted steps as the reference)
       const float yn = (float)cs->geo_yn;
       const bool want_bg = a.bg_out != nullptr;
+      // frame blocking: keep U' on chip for frame f+1 and run its pass 0 here
+      // when its normalization is already fixed (frozen statistics)
+      const bool resident = f + 1 < F && !qr;
+      const long long nfi = cs->frame_index;  // f+1's frame index (advanced by finish)
+      const bool fuse_next = resident && !(a.pipeline && !cs->frozen && nfi < a.i_init);
+      const double sd_next = a.pipeline ? (cs->frozen ? cs->pstd : running_std(cs)) : 1.0;
+      const float inv_std_n = (float)(1.0 / sd_next);
+      const size_t sox_n = sox + (size_t)ra.S * a.np;  // frame f+1's input of this stream
+      cost_n = 0.0;
+      bad_n = false;
+#pragma unroll
+      for (int j = 0; j <= K; ++j) pk_n[j] = 0.f;
       sweep([&](int qi, const auto& rows) {
         const bool ok = qi < qcount;
         const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         const size_t off = so + coord;
-        float m4[4] = {0.f, 0.f, 0.f, 0.f};  // running mean for the background, loaded first
-        if (want_bg && a.pipeline && ok && !qr) f4(*reinterpret_cast<const float4*>(Mg + off), m4);
+        float m4[4] = {0.f, 0.f, 0.f, 0.f};  // running mean, loaded first
+        if ((want_bg || fuse_next) && a.pipeline && ok && !qr) f4(*reinterpret_cast<const float4*>(Mg + off), m4);
+        float x4[4] = {0.f, 0.f, 0.f, 0.f};  // frame f+1 (fused pass 0)
+        if (fuse_next && ok) ld_x4(sox_n + coord, x4);
         float r[4], w[4], ud[4];
         f4(sR[qi], r);
         f4(sD[qi], ud);
@@ -870,10 +946,45 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #pragma unroll
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
         }
+        if (ok && a.fitres_out)
+          *reinterpret_cast<float4*>(static_cast<float*>(a.fitres_out) + fo + off) = make_float4(r[0], r[1], r[2], r[3]);
+        uint32_t nl = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (pix + e < a.P && fabsf(rr[e]) >= a.deltaf) nl |= 1u << (8 * e);
+        if (resident) {
+          // U' (and the new weights, the next frame's) back on chip
+          float wn[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            wn[e] = (ok && pix + e < a.P) ? (((nl >> (8 * e)) & 0xffu) ? omega : 1.f) : 0.f;
+          if (!WCOL && ok) sL[qi] = nl;
+          rows.template store<K>(up, wn);
+          if (fuse_next) {  // pass 0 of frame f+1: r0 = x - U'y_f (fit.py:96-104)
+            float tc = 0.f, r0[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              bad_n |= !isfinite(x4[e]);
+              float xh = a.pipeline ? __fmul_rn(__fsub_rn(x4[e], m4[e]), inv_std_n) : x4[e];
+              if (pix + e >= a.P) xh = 0.f;
+              float uu[RS];
+#pragma unroll
+              for (int j = 0; j < RS; ++j) uu[j] = j < K ? up[e][j] : 0.f;
+              r0[e] = __fsub_rn(xh, dotk<K>(uu, sfv[0]));
+              float tw, gg;
+              penalty_t<PM>(r0[e], wn[e], a, tw, gg);
+              tc += tw;
+              pk_n[K] += gg * gg;
+#pragma unroll
+              for (int j = 0; j < K; ++j) pk_n[j] += up[e][j] * gg;
+            }
+            cost_n += (double)tc;
+            sR[qi] = make_float4(r0[0], r0[1], r0[2], r0[3]);
+            sD[qi] = z4;
+          }
+        }
         if (!ok) return;
-        if (a.fitres_out)
-          *reinterpret_cast<float4*>(static_cast<float*>(a.fitres_out) + off) = make_float4(r[0], r[1], r[2], r[3]);
-        if (geo) {
+        if (geo && !resident) {
 #pragma unroll
           for (int j = 0; j < K; ++j)
             if (j < k)
@@ -881,18 +992,14 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
                      make_float4(up[0][j], up[1][j], up[2][j], up[3][j]));
         }
         if (qr) return;
-        uint32_t nl = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (pix + e < a.P && fabsf(rr[e]) >= a.deltaf) nl |= 1u << (8 * e);
         if (a.C == 1) {
           *reinterpret_cast<uint32_t*>(a.lab + (size_t)s * a.Pp + pix) = nl;
-          if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + (size_t)s * a.Pp + pix) = nl;
+          if (a.raw_out) *reinterpret_cast<uint32_t*>(a.raw_out + fl + (size_t)s * a.Pp + pix) = nl;
         } else {  // per-channel flags; k_combine3 takes the max over channels (pipeline.py:210-211)
           *reinterpret_cast<uint32_t*>(a.labc + off) = nl;
         }
         if (a.res_out)
-          *reinterpret_cast<float4*>(static_cast<float*>(a.res_out) + off) = make_float4(rr[0], rr[1], rr[2], rr[3]);
+          *reinterpret_cast<float4*>(static_cast<float*>(a.res_out) + fo + off) = make_float4(rr[0], rr[1], rr[2], rr[3]);
         if (want_bg) {
           const float sc = (float)cs->std_cur;
           float b[4];
@@ -901,17 +1008,21 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             const float bgn = dotk<K>(up[e], sfv[0]);  // U'y
             b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn * sc, m4[e]), 0.f), 1.f) : bgn;
           }
-          *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + off) = make_float4(b[0], b[1], b[2], b[3]);
+          *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + fo + off) = make_float4(b[0], b[1], b[2], b[3]);
         }
       });
+      if (resident) tmem_wait_st();
+      p0_ready = fuse_next;
     }
 
-    // ---- commit the control block (one writer per stream) ------------------
     group_sync<NG>(g);
     PHASE_MARK(PROF_T_GEO);
-#undef PHASE_MARK
     if (lt == 0) cs->pend_alpha = 0.0;
     group_sync<NG>(g);
+    }  // frames of the block
+
+    // ---- commit the control block (one writer per stream) ------------------
+#undef PHASE_MARK
     if (rank == 0 && lt < (int)(sizeof(Ctl) / 8))
       reinterpret_cast<double*>(a.ctl + s)[lt] = reinterpret_cast<const double*>(cs)[lt];
     group_sync<NG>(g);

@@ -313,12 +313,34 @@ class NativeTracker:
         self._check(rc, "push")
         return self._fit if fit else None
 
+    def push_many(self, frames, background=None, residual=None, mask=None, raw_mask=None,
+                  fit: bool = False, cuda_stream: int = 0, fit_residual=None, fit_out=None):
+        """F consecutive frames of every stream in one call — frames
+        [F, n_streams, m], outputs [F, n_streams, ...] — with each stream's
+        slice kept on chip across its F frames (prost_push_many).  The results
+        equal F calls of `push`.  With fit=True the call waits and returns the
+        F * n_streams `prost_fit_info` records (frame-major)."""
+        nf = int(frames.shape[0])
+        fp, fdt, fdev, out = self._frame_and_outputs(frames, background, residual, mask,
+                                                     raw_mask, False, fit_residual, nframes=nf)
+        fit_arr = None
+        if fit_out is not None:
+            out.fit = ctypes.cast(ctypes.c_void_p(fit_out.ptr), ctypes.POINTER(nat.FitInfo))
+            out.fit_async = 1
+        elif fit:
+            fit_arr = (nat.FitInfo * (nf * self.n_streams))()
+            out.fit = ctypes.cast(fit_arr, ctypes.POINTER(nat.FitInfo))
+        rc = self._lib.prost_push_many(self._h, fp, nf, fdt, fdev, ctypes.byref(out),
+                                       ctypes.c_void_p(cuda_stream))
+        self._check(rc, "push_many")
+        return fit_arr
+
     def _frame_and_outputs(self, frames, background, residual, mask, raw_mask, fit,
-                           fit_residual=None):
+                           fit_residual=None, nframes: int = 1):
         fp, fdt, fdev, fcount = _buffer(frames)
-        if fcount != self.n_streams * self.m:
+        if fcount != nframes * self.n_streams * self.m:
             raise DimensionError(
-                f"frames hold {fcount} values, expected {self.n_streams} x {self.m}")
+                f"frames hold {fcount} values, expected {nframes} x {self.n_streams} x {self.m}")
         out = nat.Outputs()
         dev_flags = set()
         dtype = None
@@ -328,8 +350,9 @@ class NativeTracker:
             if arr is None:
                 continue
             p, dt, dev, cnt = _buffer(arr, writable=True)
-            if cnt != self.n_streams * count:
-                raise DimensionError(f"{name} holds {cnt} values, expected {self.n_streams} x {count}")
+            if cnt != nframes * self.n_streams * count:
+                raise DimensionError(f"{name} holds {cnt} values, expected "
+                                     f"{nframes} x {self.n_streams} x {count}")
             if name in ("mask", "raw_mask"):
                 if dt != nat.U8:
                     raise ConfigError(f"{name} must be uint8")
@@ -708,6 +731,15 @@ class BatchTracker:
         return self.native.push(frames, background=background, residual=residual, mask=mask,
                                 raw_mask=raw_mask, fit=fit, cuda_stream=cuda_stream,
                                 fit_out=fit_out)
+
+    def push_many(self, frames, background=None, residual=None, mask=None, raw_mask=None,
+                  fit: bool = False, cuda_stream: int = 0, fit_out=None):
+        """F consecutive frames per stream ([F, n_streams, m]) in one launch:
+        each stream's basis stays on chip across its F frames (frame
+        blocking).  Same results as F calls of `push`."""
+        return self.native.push_many(frames, background=background, residual=residual, mask=mask,
+                                     raw_mask=raw_mask, fit=fit, cuda_stream=cuda_stream,
+                                     fit_out=fit_out)
 
     def background_frame(self, out, cuda_stream: int = 0) -> None:
         self.native.background(out, cuda_stream=cuda_stream)

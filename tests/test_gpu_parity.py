@@ -568,3 +568,57 @@ def test_off_resolution_frames_stay_on_device():
         np.testing.assert_array_equal(ra.mask.labels, rb.mask.labels)
         np.testing.assert_array_equal(ra.residual, rb.residual)
         assert ra.fit_cost == rb.fit_cost
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "u8"])
+def test_frame_blocking_matches_single_frame_pushes(dtype):
+    """push_many (F frames per stream, the slice kept on chip across them, the
+    next frame's pass 0 run inside the geodesic sweep) gives bit-identical
+    masks, raw masks, backgrounds, residuals, FitInfo and bases to pushing
+    the same frames one at a time — across the statistics window (separate
+    pass 0 there) and past it (fused)."""
+    import torch
+
+    W, H, S, F, B = 64, 48, 6, 12, 4
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=5, seed=0)
+    data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1)  # [F, S, n]
+    if dtype == "u8":
+        data = np.clip(np.rint(data * 255.0), 0, 255).astype(np.uint8)
+    else:
+        data = data.astype(np.float32)
+    one = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    blk = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    n = W * H
+    ref = {k: [] for k in ("mask", "raw", "bg", "res", "cost", "fi")}
+    m1 = torch.empty((S, n), dtype=torch.uint8, device="cuda")
+    r1 = torch.empty((S, n), dtype=torch.uint8, device="cuda")
+    b1 = torch.empty((S, n), dtype=torch.float32, device="cuda")
+    e1 = torch.empty((S, n), dtype=torch.float32, device="cuda")
+    for f in range(F):
+        info = one.push(torch.from_numpy(data[f]).cuda(), background=b1, residual=e1, mask=m1,
+                        raw_mask=r1, fit=True)
+        ref["mask"].append(m1.cpu().numpy())
+        ref["raw"].append(r1.cpu().numpy())
+        ref["bg"].append(b1.cpu().numpy())
+        ref["res"].append(e1.cpu().numpy())
+        ref["cost"].append([info[s].fit_cost for s in range(S)])
+        ref["fi"].append([info[s].frame_index for s in range(S)])
+    mb = torch.empty((B, S, n), dtype=torch.uint8, device="cuda")
+    rb = torch.empty((B, S, n), dtype=torch.uint8, device="cuda")
+    bb = torch.empty((B, S, n), dtype=torch.float32, device="cuda")
+    eb = torch.empty((B, S, n), dtype=torch.float32, device="cuda")
+    for f0 in range(0, F, B):
+        info = blk.push_many(torch.from_numpy(data[f0:f0 + B]).cuda(), background=bb, residual=eb,
+                             mask=mb, raw_mask=rb, fit=True)
+        for i in range(B):
+            f = f0 + i
+            np.testing.assert_array_equal(mb[i].cpu().numpy(), ref["mask"][f])
+            np.testing.assert_array_equal(rb[i].cpu().numpy(), ref["raw"][f])
+            np.testing.assert_array_equal(bb[i].cpu().numpy(), ref["bg"][f])
+            np.testing.assert_array_equal(eb[i].cpu().numpy(), ref["res"][f])
+            assert [info[i * S + s].fit_cost for s in range(S)] == ref["cost"][f]
+            assert [info[i * S + s].frame_index for s in range(S)] == ref["fi"][f]
+    for s in range(S):
+        np.testing.assert_array_equal(blk.native.get_core_state(s)[0], one.native.get_core_state(s)[0])
