@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--e2e-f32", action="store_true",
                     help="end-to-end leg with fp32 frames instead of 8-bit camera frames")
     ap.add_argument("--wave", type=int, default=0)
+    ap.add_argument("--block", type=int, default=8,
+                    help="also time frame-blocked pushes (push_many) of this many frames per "
+                         "stream per call; 0 or 1: skip")
     ap.add_argument("--pixel-shard", action="store_true",
                     help="shard one stream's pixel rows over the ranks (default for C4 with N > 1)")
     ap.add_argument("--preroll", type=int, default=None,
@@ -335,7 +338,8 @@ def main():
 
     preroll = cfg.i_init if args.preroll is None else args.preroll
     e2e_frames = 0 if args.no_e2e else 2 + args.steps
-    need = preroll + args.warmup + args.steps + 3 + e2e_frames
+    nblock = 0 if args.block <= 1 else args.block * (max(1, args.steps // args.block) + 1)
+    need = preroll + args.warmup + args.steps + 3 + e2e_frames + nblock
     t_gen = time.perf_counter()
     if args.frames > 0:
         # a few distinct frames, cycled (numpy generator, bit-identical to the tests' streams)
@@ -455,6 +459,33 @@ def main():
     ms_step = ms / args.steps
     units = S if pixel else ws * S  # stream-frames of the whole job
     value = units * args.steps / (ms / 1000.0)
+
+    # frame blocking (BatchTracker.push_many): the same streams continue, F
+    # consecutive frames per stream per call, each stream's slice kept on chip
+    # across its F frames — the same per-frame results (tested bit-identical)
+    blocked = None
+    FB = args.block if (not pixel and args.block and args.block > 1 and host is None) else 0
+    if FB:
+        bg_b = torch.empty((FB,) + tuple(bg.shape), dtype=bg.dtype, device=bg.device)
+        mask_b = torch.empty((FB,) + tuple(mask.shape), dtype=mask.dtype, device=mask.device)
+        reps = max(1, args.steps // FB)
+        bt.push_many(frames_dev[step:step + FB], background=bg_b, mask=mask_b)
+        step += FB
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(reps):
+            bt.push_many(frames_dev[step:step + FB], background=bg_b, mask=mask_b)
+            step += FB
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_b = max_over_ranks(e0.elapsed_time(e1)) / (reps * FB)
+        blocked = {"frames_per_call": FB, "value": units / (ms_b / 1000.0), "unit": "stream-frames/s",
+                   "ms_per_frame_step": ms_b, "steps": reps * FB,
+                   "hbm_bytes_per_stream_frame": 8 * n_loc * k / FB + 12 * n_loc + 3 * P_loc,
+                   "note": "BatchTracker.push_many: U crosses HBM once per block of F frames "
+                           "(per-frame results identical to push; tests/test_gpu_parity.py)"}
 
     # per-phase breakdown (separate, untimed pass with events around launches)
     native.profile(True)
@@ -601,6 +632,7 @@ def main():
             "cpu_baseline": cpu,
             "gen_seconds": t_gen,
             "exchanges_per_frame": ex_timed,
+            "blocked": blocked,
             "preroll": {"frames": preroll, "seconds": t_pre,
                         "note": "untimed frames through the i_init statistics window before warm-up; "
                                 "the timed steps are steady-state frames (90% of a 1000-frame run)"},

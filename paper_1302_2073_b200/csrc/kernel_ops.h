@@ -36,6 +36,6 @@ struct TmOps {
   int ng;  // slot groups per CTA
   void (*describe)();
 };
-TmOps pick_tmem(int K, bool half, int ng);
+TmOps pick_tmem(int K, bool half, int ng, bool blk = false);
 
 }  // namespace prost_ops

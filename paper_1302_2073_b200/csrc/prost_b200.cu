@@ -896,7 +896,8 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
       if ((nq + qpc - 1) / qpc != G) continue;
       const size_t sm = to.smem(qpc);
       if (sm > (size_t)227 * 1024) continue;
-      const bool set = to.prepare(sm) == cudaSuccess;  // before the occupancy query
+      const TmOps tb = pick_tmem(K, params->p == 0.5, ng, true);  // frame-blocking instance
+      const bool set = to.prepare(sm) == cudaSuccess && (!tb.prepare || tb.prepare(sm) == cudaSuccess);
       const bool fits = set && (TM_CPS == 1 ? to.occupancy(sm) >= 1
                                             : (size_t)TM_CPS * (sm + 2048) <= (size_t)228 * 1024);
       if (!fits) {
@@ -1288,7 +1289,7 @@ int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_
   CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
   {
     PhaseTimer pt_(h, st, PROST_PH_FRAME);
-    CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng).launch(a, ra, h->rsmem, st));
+    CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng, true).launch(a, ra, h->rsmem, st));
   }
   h->launches += 1;
   if (o.mask) {

@@ -294,7 +294,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 // frames, so one group's HBM traffic (slice load, U' store) and its team-sum
 // latency overlap the other group's sweeps (optionally enforced: ra.alt makes
 // the groups' slice loads alternate A, B, A, B, ...).
-template <int K, int PM, int NG>
+// BLK: the frame-blocking instance (prost_push_many); the single-frame
+// instance compiles the blocking paths out (they cost registers).
+template <int K, int PM, int NG, bool BLK>
 __global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     // updated (r0 = x_{f+1} - U'y_f: the warm start is this frame's y), and
     // the per-frame outputs go to [f][S][...].  Every frame computes exactly
     // what one push per frame computes.
-    const int F = (a.nframes > 1 && a.C == 1) ? a.nframes : 1;
+    const int F = (BLK && a.nframes > 1 && a.C == 1) ? a.nframes : 1;
     bool p0_ready = false;  // this frame's pass 0 partials came with the last geodesic sweep
     double cost_n = 0.0;
     bool bad_n = false;
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     const bool frame_ok = cs->status == ST_OK;
     const bool cold = frame_ok && cs->frame_index == 0;
     const bool fuse = frame_ok && !cold;
-    const bool use_p0 = f > 0 && p0_ready && frame_ok && !upd;
+    const bool use_p0 = BLK && f > 0 && p0_ready && frame_ok && !upd;
     bool bad = use_p0 ? bad_n : false;
     bool mean_pending = upd;  // running-mean update not yet written this frame
     double cost = use_p0 ? cost_n : 0.0;
@@ -903,7 +905,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       const bool want_bg = a.bg_out != nullptr;
       // frame blocking: keep U' on chip for frame f+1 and run its pass 0 here
       // when its normalization is already fixed (frozen statistics)
-      const bool resident = f + 1 < F && !qr;
+      const bool resident = BLK && f + 1 < F && !qr;
       const long long nfi = cs->frame_index;  // f+1's frame index (advanced by finish)
       const bool fuse_next = resident && !(a.pipeline && !cs->frozen && nfi < a.i_init);
       const double sd_next = a.pipeline ? (cs->frozen ? cs->pstd : running_std(cs)) : 1.0;

@@ -1,5 +1,5 @@
-// tmem_k.cu — instances of the TMEM-resident frame kernel k_tmem
-// (prost_tmem.cuh) and their launchers (kernel_ops.h).
+// tmem_blk_k.cu — the frame-blocking instances of k_tmem (prost_push_many),
+// in their own translation unit so the library builds in parallel.
 #include <cstdio>
 
 #include "kernel_ops.h"
@@ -59,13 +59,6 @@ TmOps pick_blk(int K, bool half) {
   }
 }
 
-TmOps pick_tmem_blocking(int K, bool half);  // tmem_blk_k.cu
-
-TmOps pick_tmem(int K, bool half, int ng, bool blk) {
-  // NG = 2 (two streams per CTA in parallel warp groups) measured slower on
-  // C3: the launcher keeps the template, only NG = 1 is built
-  if (ng != 1) return TmOps{nullptr, nullptr, nullptr, nullptr, 0, ng, nullptr};
-  return blk ? pick_tmem_blocking(K, half) : pick_blk<false>(K, half);
-}
+TmOps pick_tmem_blocking(int K, bool half) { return pick_blk<true>(K, half); }
 
 }  // namespace prost_ops
