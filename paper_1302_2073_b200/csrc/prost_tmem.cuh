@@ -93,7 +93,7 @@ __host__ __device__ constexpr size_t tmem_group_smem(int qpc) {
   const int qs = qpc > Geo::QT * TG ? qpc - Geo::QT * TG : 0;
   const int qa = (qpc + TG - 1) / TG * TG;  // r / u_dir arrays cover whole slots
   return ((size_t)16 * Geo::RS * qs        // basis row groups kept in shared memory
-          + (size_t)qa * 32                // r, u_dir
+          + (size_t)qa * 48                // r, u_dir, U y
           + (Geo::WCOL ? 0 : (size_t)qa * 4)  // label words
           + (size_t)(TG / 32 + 1) * Geo::NV * 8 + sizeof(Ctl) + 127) / 128 * 128;
 }
@@ -333,7 +333,12 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   float4* sU = reinterpret_cast<float4*>(smem_raw + (size_t)g * tmem_group_smem<K, NG>(qpc));  // [4][RS/4][qs]
   float4* sR = sU + (size_t)RS * qs;                    // [qa] residual
   float4* sD = sR + qa;                                 // [qa] u_dir
-  uint32_t* sL = reinterpret_cast<uint32_t*>(sD + qa);  // [qa] label bytes (!WCOL)
+  // [qa] U y at the current coordinates: pass 0's dot, then every accepted
+  // step adds alpha * u_dir (the residual's recurrence, fit.py:136).  The
+  // geodesic sweep gets U v = U y / ||y|| and the background U'y = U y +
+  // coef ||y|| from it instead of two more k-term dot products per row.
+  float4* sY = sD + qa;
+  uint32_t* sL = reinterpret_cast<uint32_t*>(sY + qa);  // [qa] label bytes (!WCOL)
   double* wred = reinterpret_cast<double*>(sL + (WCOL ? 0 : qa));
   double* red = wred + (size_t)(TG / 32) * NVM;
   Ctl* cs = reinterpret_cast<Ctl*>(red + NVM);
@@ -609,7 +614,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + coord)) : z4;
         const uint32_t lb = ok ? *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + pix) : 0u;
         if (!WCOL) sL[qi] = lb;
-        float xh[4], w[4], r[4];
+        float xh[4], w[4], r[4], uy[4];
         if (fuse) xhat(qi, mean_pending, xh, bad);
 #pragma unroll
         for (int e = 0; e < 4; ++e)
@@ -633,7 +638,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
               rp[(size_t)g4 * qs] = make_float4(row[4 * g4], row[4 * g4 + 1], row[4 * g4 + 2], row[4 * g4 + 3]);
           }
           if (fuse) {
-            r[e] = __fsub_rn(xh[e], dotk<K>(row, sfv[0]));
+            uy[e] = dotk<K>(row, sfv[0]);
+            r[e] = __fsub_rn(xh[e], uy[e]);
             float tw, gg;
             penalty_t<PM>(r[e], w[e], a, tw, gg);
             tc += tw;
@@ -646,6 +652,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           cost += (double)tc;
           sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
           sD[qi] = z4;
+          sY[qi] = make_float4(uy[0], uy[1], uy[2], uy[3]);
         }
       }
       tmem_wait_st();
@@ -690,7 +697,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         }
         if (cs->status == ST_OK) {
           sweep([&](int qi, const auto& rows) {
-            float xh[4], w[4], r[4];
+            float xh[4], w[4], r[4], uy[4];
             xhat(qi, mean_pending, xh, bad);
             if (!WCOL) lab_weights(qi, w);
             float tc = 0.f;
@@ -699,7 +706,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
               float u[RS];
               rows(e, u);
               if (WCOL) w[e] = u[RS - 1];
-              r[e] = __fsub_rn(xh[e], dotk<K>(u, sfv[0]));
+              uy[e] = dotk<K>(u, sfv[0]);
+              r[e] = __fsub_rn(xh[e], uy[e]);
               float tw, gg;
               penalty_t<PM>(r[e], w[e], a, tw, gg);
               tc += tw;
@@ -710,6 +718,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             cost += (double)tc;
             sR[qi] = make_float4(r[0], r[1], r[2], r[3]);
             sD[qi] = z4;
+            sY[qi] = make_float4(uy[0], uy[1], uy[2], uy[3]);
           });
         }
       }
@@ -824,6 +833,13 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           float r[4], w[4], udo[4], ud[4];
           f4(sR[qi], r);
           f4(sD[qi], udo);
+          if (pa != 0.f) {  // the pending accepted step moves U y too
+            float y4[4];
+            f4(sY[qi], y4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) y4[e] = fmaf(pa, udo[e], y4[e]);
+            sY[qi] = make_float4(y4[0], y4[1], y4[2], y4[3]);
+          }
           if (!WCOL) lab_weights(qi, w);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -902,6 +918,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       // the fit residual x - U y kept on chip (fit.py's res, the same
       // recurrence of accepted steps as the reference)
       const float yn = (float)cs->geo_yn;
+      const float inv_yn = geo ? (float)(1.0 / cs->geo_yn) : 0.f;
       const bool want_bg = a.bg_out != nullptr;
       // frame blocking: keep U' on chip for frame f+1 and run its pass 0 here
       // when its normalization is already fixed (frozen statistics)
@@ -923,28 +940,31 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         if ((want_bg || fuse_next) && a.pipeline && ok && !qr) f4(*reinterpret_cast<const float4*>(Mg + off), m4);
         float x4[4] = {0.f, 0.f, 0.f, 0.f};  // frame f+1 (fused pass 0)
         if (fuse_next && ok) ld_x4(sox_n + coord, x4);
-        float r[4], w[4], ud[4];
+        float r[4], w[4], ud[4], uy[4];
         f4(sR[qi], r);
         f4(sD[qi], ud);
+        f4(sY[qi], uy);
         if (!WCOL) lab_weights(qi, w);
         float up[4][K];  // U' rows of this row group
-        float rr[4];
+        float rr[4], bgn[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float u[RS];
           rows(e, u);
           if (WCOL) w[e] = u[RS - 1];
           r[e] = trial(r[e], pa, ud[e]);  // the fit residual x - U y (fit.py res)
+          uy[e] = fmaf(pa, ud[e], uy[e]);  // U y at the fitted y
           float coef = 0.f;
           if (geo) {
             float tw, g;
             penalty_t<PM>(r[e], w[e], a, tw, g);
             const float eta = -g;  // cost.py:103-112
-            const float uv = dotk<K>(u, sfv[2]);
+            const float uv = uy[e] * inv_yn;  // U v, v = y / ||y||
             const float ug = dotk<K>(u, sfv[3]);
             coef = ga * uv - gsn * ((eta - ug) * inv_ln);
           }
           rr[e] = fmaf(-coef, yn, r[e]);
+          bgn[e] = fmaf(coef, yn, uy[e]);  // U'y = U y + coef ||y||
 #pragma unroll
           for (int j = 0; j < K; ++j) up[e][j] = u[j] + coef * sfv[2][j];
         }
@@ -963,7 +983,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           if (!WCOL && ok) sL[qi] = nl;
           rows.template store<K>(up, wn);
           if (fuse_next) {  // pass 0 of frame f+1: r0 = x - U'y_f (fit.py:96-104)
-            float tc = 0.f, r0[4];
+            float tc = 0.f, r0[4], uy0[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               bad_n |= !isfinite(x4[e]);
@@ -972,7 +992,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
               float uu[RS];
 #pragma unroll
               for (int j = 0; j < RS; ++j) uu[j] = j < K ? up[e][j] : 0.f;
-              r0[e] = __fsub_rn(xh, dotk<K>(uu, sfv[0]));
+              uy0[e] = dotk<K>(uu, sfv[0]);  // a fresh dot, as the next push's pass 0
+              r0[e] = __fsub_rn(xh, uy0[e]);
               float tw, gg;
               penalty_t<PM>(r0[e], wn[e], a, tw, gg);
               tc += tw;
@@ -983,6 +1004,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             cost_n += (double)tc;
             sR[qi] = make_float4(r0[0], r0[1], r0[2], r0[3]);
             sD[qi] = z4;
+            sY[qi] = make_float4(uy0[0], uy0[1], uy0[2], uy0[3]);
           }
         }
         if (!ok) return;
@@ -1006,10 +1028,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           const float sc = (float)cs->std_cur;
           float b[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float bgn = dotk<K>(up[e], sfv[0]);  // U'y
-            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn * sc, m4[e]), 0.f), 1.f) : bgn;
-          }
+          for (int e = 0; e < 4; ++e)
+            b[e] = a.pipeline ? fminf(fmaxf(__fadd_rn(bgn[e] * sc, m4[e]), 0.f), 1.f) : bgn[e];
           *reinterpret_cast<float4*>(static_cast<float*>(a.bg_out) + fo + off) = make_float4(b[0], b[1], b[2], b[3]);
         }
       });
