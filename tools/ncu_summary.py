@@ -50,7 +50,13 @@ def launches(path):
 
 
 def rep(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Key metrics of a full capture: an .ncu-rep, or its raw-page CSV export
+    (tools/ncu_src.sh writes gpurun_out/ncu_raw.csv on the box)."""
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -65,6 +71,41 @@ def rep(path):
     return res
 
 
+def sass_mix(path, top=14):
+    """Executed-instruction mix by opcode and stall reasons (whole kernel)."""
+    rows = list(csv.reader(open(path)))
+    hdr = rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    data = [r for r in rows[2:] if len(r) >= len(hdr)]
+
+    def num(x):
+        try:
+            return int(x)
+        except ValueError:
+            return 0
+    ops = collections.Counter()
+    stalls = collections.Counter()
+    scols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+    for r in data:
+        op = r[idx["Source"]].strip().split()
+        if not op:
+            continue
+        o = op[1] if op[0].startswith("@") and len(op) > 1 else op[0]
+        ops[o.split(".")[0]] += num(r[idx["Instructions Executed"]])
+        for h in scols:
+            stalls[h[6:]] += num(r[idx[h]])
+    ti, ts = sum(ops.values()) or 1, sum(stalls.values()) or 1
+    out = ["## SASS mix and stall reasons (whole kernel)", "",
+           f"warp instructions executed: {ti:,}", "",
+           "| opcode | share of instructions |", "|---|---|"]
+    out += [f"| {k} | {v / ti:.3f} |" for k, v in ops.most_common(top)]
+    out += ["", "| stall reason | share of samples |", "|---|---|"]
+    out += [f"| {k} | {v / ts:.3f} |" for k, v in stalls.most_common(10)]
+    tma = [k for k in ops if k.startswith(("UTMA", "UBLK"))]
+    out += ["", f"TMA / bulk-copy opcodes present: {', '.join(tma) if tma else 'none'}", ""]
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
@@ -72,6 +113,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--title", default="ncu summary")
     ap.add_argument("--note", default="")
+    ap.add_argument("--sass", default=None, help="SASS source-page CSV: opcode mix + stall reasons")
     a = ap.parse_args()
     lines = [f"# {a.title}", ""]
     if a.note:
@@ -80,7 +122,7 @@ def main():
         agg = launches(a.launches)
         # only this library's kernels: the benchmark's input generation (torch
         # / cuBLAS) runs before the timed region
-        agg = collections.OrderedDict((k, v) for k, v in agg.items() if k.startswith("prost::"))
+        agg = collections.OrderedDict((k, v) for k, v in agg.items() if k.split("::")[-1].startswith("k_"))
         tot = sum(sum(v) for v in agg.values()) or 1.0
         lines += ["## Launch list (ncu `gpu__time_duration.sum`, `--clock-control none`; cold-cache, serialised)", "",
                   "| kernel | launches | avg us | total us | share | DRAM MB / launch |",
@@ -96,6 +138,8 @@ def main():
             lines += [f"## `{kn.split('(')[0]}` (`ncu --set full`, {r.split('/')[-1]})", "", "| metric | value |", "|---|---|"]
             lines += [f"| {k} | {v} |" for k, v in d.items()]
             lines.append("")
+    if a.sass:
+        lines += sass_mix(a.sass)
     open(a.out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
