@@ -7,6 +7,7 @@
 // cold start) is decided on the device: kernels whose condition is false for
 // a stream exit immediately, so the host never synchronizes inside a frame.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,12 +16,14 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/prost_b200.h"
 #include "prost_phases.cuh"
 #include "prost_resident.cuh"
 #include "prost_tmem.cuh"
+#include "prost_stream_tma.cuh"
 #include "kernel_ops.h"
 
 using namespace prost;
@@ -63,6 +66,11 @@ struct prost_handle {
   double* rpart = nullptr;
   unsigned long long* rprof = nullptr;
   int resident_ops_K = 0;
+  // streamed fp32 one-channel k > 20 (BASELINE C4): pass 0 / iteration /
+  // gradient passes fed by tensor copies of U (prost_stream_tma.cuh)
+  bool tma = false;
+  int tma_chunks = 0;
+  CUtensorMap umap{};
   // device state
   void* U = nullptr;
   void* r = nullptr;
@@ -292,13 +300,34 @@ struct Impl {
     long long n = 0;
     LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a)));
     if (h->maybe_cold) LAUNCH(PROST_PH_COLD, (k_cold<T, K, VEC><<<grid, NT, 0, st>>>(a)));
-    LAUNCH(PROST_PH_PASS0, (k_pass0<T, K, VEC><<<grid, NT, 0, st>>>(a)));
-    for (int it = 0; it < h->prm.cg_max_iters; ++it) {
-      LAUNCH(PROST_PH_ITER, (k_iter<T, K, VEC><<<grid, NT, 0, st>>>(a)));
-      for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
-      LAUNCH(PROST_PH_GRADFB, (k_gradfb<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    // tensor-copy-fed U passes (prost_stream_tma.cuh): frame pointer aligned
+    // for the 1-D bulk copies
+    bool fed = false;
+    if constexpr (std::is_same<T, float>::value && K > 20) {
+      if (h->tma && ((uintptr_t)a.x & 15) == 0) {
+        fed = true;
+        Args at = a;
+        at.chunks = h->tma_chunks;
+        const dim3 tg(h->tma_chunks, sw);
+        constexpr size_t sm = tma_smem_small<K>(), sg = tma_smem_geo<K>();
+        LAUNCH(PROST_PH_PASS0, (k_pass0_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
+        for (int it = 0; it < h->prm.cg_max_iters; ++it) {
+          LAUNCH(PROST_PH_ITER, (k_iter_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
+          for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
+          LAUNCH(PROST_PH_GRADFB, (k_gradfb_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
+        }
+        LAUNCH(PROST_PH_GEO, (k_geo_tma<K><<<tg, TT, sg, st>>>(at, h->umap)));
+      }
     }
-    LAUNCH(PROST_PH_GEO, (k_geo<T, K, VEC, false><<<grid, NT, 0, st>>>(a)));
+    if (!fed) {
+      LAUNCH(PROST_PH_PASS0, (k_pass0<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+      for (int it = 0; it < h->prm.cg_max_iters; ++it) {
+        LAUNCH(PROST_PH_ITER, (k_iter<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+        for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
+        LAUNCH(PROST_PH_GRADFB, (k_gradfb<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+      }
+      LAUNCH(PROST_PH_GEO, (k_geo<T, K, VEC, false><<<grid, NT, 0, st>>>(a)));
+    }
     if (h->qr_due) {
       LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
       LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
@@ -343,6 +372,55 @@ struct Impl {
     h->launches += 1;
   }
 };
+
+// Tensor map of the basis planes, [S*k rows][np coordinates] fp32, read in
+// boxes of k rows x TBOX coordinates (prost_stream_tma.cuh).  The driver entry
+// point is looked up at run time (no -lcuda).  PROST_TMA=0 keeps the plain
+// streamed kernels.
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <int K>
+bool tma_attrs() {
+  const int sm = (int)tma_smem_small<K>(), sg = (int)tma_smem_geo<K>();
+  return cudaFuncSetAttribute(k_pass0_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess &&
+         cudaFuncSetAttribute(k_iter_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess &&
+         cudaFuncSetAttribute(k_gradfb_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess &&
+         cudaFuncSetAttribute(k_geo_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg) == cudaSuccess;
+}
+
+void setup_tma(prost_handle* h, int sms) {
+  const char* env = getenv("PROST_TMA");
+  if ((env && env[0] == '0') || h->Pp % 16 != 0) return;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)h->np, (cuuint64_t)h->S * h->k};
+  const cuuint64_t strides[1] = {(cuuint64_t)h->np * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)TBOX, (cuuint32_t)h->k};
+  const cuuint32_t estr[2] = {1, 1};
+  if (reinterpret_cast<EncodeTiled>(fn)(&h->umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, h->U, dims, strides, box, estr,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  const bool ok = h->ops.K == 30 ? tma_attrs<30>() : h->ops.K == 32 ? tma_attrs<32>() : false;
+  if (!ok) {
+    cudaGetLastError();
+    return;
+  }
+  // one CTA per SM (the tile ring takes most of shared memory), at most the
+  // part slots the plain kernels use, at least one tile per CTA
+  const long long tiles = (h->Pp + TT - 1) / TT;
+  const long long per = std::max<long long>(1, (long long)sms / h->S);
+  h->tma_chunks = (int)std::max<long long>(1, std::min<long long>({per, tiles, (long long)h->chunks}));
+  h->tma = true;
+}
 
 template <typename T>
 Ops pick(int k) {
@@ -839,6 +917,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   CK(cudaMallocHost(&h->info_h, S * sizeof(FitInfo)));
   CK(cudaMallocHost(&h->info_peek, S * sizeof(FitInfo)));
   CK(cudaEventCreateWithFlags(&h->ev_peek, cudaEventDisableTiming));
+  if (!h->fp64 && h->C == 1 && K > 20) setup_tma(h, sms);
   // Resident frame kernel: fp32, one channel, k <= 16, and a team that fits the
   // chip.  The geometry depends on the stream shape only (not on n_streams), so
   // a stream's reduction order — and its result — is the same in any batch.

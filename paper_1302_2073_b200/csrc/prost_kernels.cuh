@@ -267,6 +267,8 @@ __device__ __forceinline__ double warp_sum(double x) {
 }
 
 // Reduce one per-thread value over the CTA into sm[warp][slot] (lane 0 writes).
+// NTH: threads of the CTA (the TMA-fed streamed kernels run 512).
+template <int NTH = NT>
 __device__ __forceinline__ void cta_stage(double x, double* sm, int slot, int nv) {
   x = warp_sum(x);
   if ((threadIdx.x & 31) == 0) sm[(threadIdx.x >> 5) * nv + slot] = x;
@@ -275,13 +277,15 @@ __device__ __forceinline__ void cta_stage(double x, double* sm, int slot, int nv
 // Finish the CTA reduction: sum warps in order into this CTA's partial slot,
 // then arrive; returns true in the last CTA of the stream, whose `red` holds
 // the stream-wide sums (slots summed in slot order).
+template <int NTH = NT>
 __device__ __forceinline__ bool cta_finish(const Args& a, int s, double* sm, int nv, double* red) {
+  constexpr int NWL = NTH / 32;
   __shared__ int last;
   double* slot = a.part + ((size_t)s * a.chunks + blockIdx.x) * a.nvmax;
   __syncthreads();
-  for (int v = threadIdx.x; v < nv; v += NT) {
+  for (int v = threadIdx.x; v < nv; v += NTH) {
     double acc = 0.0;
-    for (int w = 0; w < NW; ++w) acc += sm[w * nv + v];
+    for (int w = 0; w < NWL; ++w) acc += sm[w * nv + v];
     slot[v] = acc;
   }
   __threadfence();
@@ -298,26 +302,26 @@ __device__ __forceinline__ bool cta_finish(const Args& a, int s, double* sm, int
   // (32 at a time), warp w = chunks w, w + NW, ... (four independent loads in
   // flight per lane), then the NW warp sums in warp order.
   const double* base = a.part + (size_t)s * a.chunks * a.nvmax;
-  __shared__ double wsum[NW][32];
+  __shared__ double wsum[NWL][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int v0 = 0; v0 < nv; v0 += 32) {
     const int v = v0 + lane;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     if (v < nv) {
       int c = warp;
-      for (; c + 3 * NW < a.chunks; c += 4 * NW) {
+      for (; c + 3 * NWL < a.chunks; c += 4 * NWL) {
         acc0 += __ldcg(base + (size_t)c * a.nvmax + v);
-        acc1 += __ldcg(base + (size_t)(c + NW) * a.nvmax + v);
-        acc2 += __ldcg(base + (size_t)(c + 2 * NW) * a.nvmax + v);
-        acc3 += __ldcg(base + (size_t)(c + 3 * NW) * a.nvmax + v);
+        acc1 += __ldcg(base + (size_t)(c + NWL) * a.nvmax + v);
+        acc2 += __ldcg(base + (size_t)(c + 2 * NWL) * a.nvmax + v);
+        acc3 += __ldcg(base + (size_t)(c + 3 * NWL) * a.nvmax + v);
       }
-      for (; c < a.chunks; c += NW) acc0 += __ldcg(base + (size_t)c * a.nvmax + v);
+      for (; c < a.chunks; c += NWL) acc0 += __ldcg(base + (size_t)c * a.nvmax + v);
     }
     wsum[warp][lane] = (acc0 + acc1) + (acc2 + acc3);
     __syncthreads();
     if (warp == 0 && v < nv) {
       double acc = 0.0;
-      for (int w = 0; w < NW; ++w) acc += wsum[w][lane];
+      for (int w = 0; w < NWL; ++w) acc += wsum[w][lane];
       red[v] = acc;
       if (a.xred) a.xred[(size_t)s * a.nvmax + v] = acc;  // exchange mode: k_xlogic finishes
     }
