@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--block", type=int, default=8,
                     help="also time frame-blocked pushes (push_many) of this many frames per "
                          "stream per call; 0 or 1: skip")
+    ap.add_argument("--exchange", choices=["peer", "program"], default="peer",
+                    help="pixel sharding: in-kernel exchange over peer memory (peer) or the "
+                         "host-driven all-reduce program (program)")
     ap.add_argument("--pixel-shard", action="store_true",
                     help="shard one stream's pixel rows over the ranks (default for C4 with N > 1)")
     ap.add_argument("--preroll", type=int, default=None,
@@ -375,7 +378,7 @@ def main():
     if pixel:
         from paper_1302_2073_b200.shard import ShardedTracker
 
-        st = ShardedTracker(cfg, precision=args.precision, device=dev)
+        st = ShardedTracker(cfg, precision=args.precision, device=dev, exchange=args.exchange)
         native = st.native
         W_, r0, r1 = W, st.row0, st.row1
         # this rank's row block of every staged frame
@@ -399,7 +402,9 @@ def main():
     mode = native.query(nat.Q_RESIDENT)
     if pixel:
         kernel_path = (f"pixel-sharded: rows {r0}-{r1} of {H} on rank {rank}, streamed phase "
-                       f"kernels, NCCL all-reduce of the phase partials")
+                       + ("kernels exchanging their partials in-kernel over peer memory"
+                          if args.exchange == "peer" else
+                          "kernels, NCCL all-reduce of the phase partials (host-driven program)"))
     elif mode:
         kernel_path = (f"{'tmem' if mode == 2 else 'register'}-resident: "
                        f"{native.query(nat.Q_TEAMS)} teams x "
@@ -439,7 +444,12 @@ def main():
     clocks.start()
     time.sleep(0.3)
     launches0 = native.launches
-    ex0 = st.exchanges if pixel else 0
+    def exchanges_so_far():
+        if not pixel:
+            return 0
+        return st.peer_exchanges() if args.exchange == "peer" else st.exchanges
+
+    ex0 = exchanges_so_far()
     barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -453,7 +463,7 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1)
     launches = native.launches - launches0
-    ex_timed = (st.exchanges - ex0) / args.steps if pixel else None
+    ex_timed = (exchanges_so_far() - ex0) / args.steps if pixel else None
     clk = clocks.stop()
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps

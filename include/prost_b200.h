@@ -178,6 +178,7 @@ int prost_last_error(prost_handle* h, char* buf, int32_t len);
 #define PROST_Q_TEAMS 7      /* teams (resident mode) */
 #define PROST_Q_GROUPS 8     /* slot groups per CTA of the TMEM kernel: streams per team in flight */
 #define PROST_Q_QPC 9        /* row groups (4 coordinates) per CTA slice (resident modes) */
+#define PROST_Q_EXCHANGES 10 /* in-kernel cross-rank exchanges of stream 0 so far (peer mode) */
 int prost_query(prost_handle* h, int32_t what, int64_t* value);
 
 /* Per-phase device timing (CUDA events around every launch, on the launch
@@ -255,6 +256,24 @@ int prost_xapply(prost_handle* h, void* cuda_stream);
 int prost_xedges(prost_handle* h, uint8_t* top, uint8_t* bottom, void* cuda_stream);  /* [S][width] */
 int prost_xfinish(prost_handle* h, const uint8_t* halo_top, const uint8_t* halo_bottom,
                   void* cuda_stream);
+
+/* Pixel sharding with the exchange inside the kernels (the
+ * compute step and its collective fused over NVLink peer memory).  Instead of
+ * the host-driven program above, every rank of an exchange-mode handle
+ *
+ *   prost_xpeer_handle(h, world, handle)          64-byte IPC handle of its exchange region
+ *   (all-gather the handles over the ranks, e.g. torch.distributed)
+ *   prost_xpeer_open(h, rank, world, handles)     map every rank's region
+ *
+ * after which prost_push(h, this rank's row block, ...) runs the whole frame:
+ * the last CTA of each phase kernel stores the stream's sums into every rank's
+ * region, waits for every rank's flag and sums them in rank order; phases that
+ * do not run for the stream (fallbacks, statistics after the window) exchange
+ * nothing.  The median takes its halo rows from the neighbours' stores.  Every
+ * rank must push every frame (the kernels wait for each other). */
+#define PROST_IPC_HANDLE_BYTES 64
+int prost_xpeer_handle(prost_handle* h, int32_t world, void* ipc_handle);
+int prost_xpeer_open(prost_handle* h, int32_t rank, int32_t world, const void* ipc_handles);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,8 @@ F32, F64, U8 = 0, 1, 2
 FLAG_PIPELINE, FLAG_FP64, FLAG_LATENCY = 1, 2, 4
 Q_LAUNCHES, Q_WAVE, Q_BYTES_U, Q_CHUNKS, Q_INSTANCE_K = 0, 1, 2, 3, 4
 Q_RESIDENT, Q_TEAM, Q_TEAMS, Q_GROUPS, Q_QPC = 5, 6, 7, 8, 9
+Q_EXCHANGES = 10
+IPC_HANDLE_BYTES = 64
 
 EXPORTS = (
     "prost_abi_version", "prost_create", "prost_destroy", "prost_set_core_state",
@@ -30,7 +32,7 @@ EXPORTS = (
     "prost_background", "prost_synchronize", "prost_last_error", "prost_query",
     "prost_set_wave", "prost_profile", "prost_profile_read", "prost_resident_counters",
     "prost_set_exchange", "prost_xbuffer", "prost_xbegin", "prost_xnext", "prost_xapply",
-    "prost_xedges", "prost_xfinish", "prost_join", "prost_resample", "prost_upsample_mask",
+    "prost_xedges", "prost_xfinish", "prost_xpeer_handle", "prost_xpeer_open", "prost_join", "prost_resample", "prost_upsample_mask",
     "prost_confusion", "prost_unpack_pnm",
 )
 PHASES = ("stats", "cold", "pass0", "iter", "lsfb", "gradfb", "geo", "qr", "median", "frame")
@@ -117,6 +119,8 @@ def lib() -> ctypes.CDLL:
     L.prost_xapply.argtypes = [vp, vp]
     L.prost_xedges.argtypes = [vp, vp, vp, vp]
     L.prost_xfinish.argtypes = [vp, vp, vp, vp]
+    L.prost_xpeer_handle.argtypes = [vp, i32, vp]
+    L.prost_xpeer_open.argtypes = [vp, i32, i32, vp]
     L.prost_join.argtypes = [vp, vp]
     L.prost_resample.argtypes = [vp, i32, i32, i32, i32, vp, i32, i32, i32, vp]
     L.prost_upsample_mask.argtypes = [vp, i32, i32, vp, i32, i32, vp]

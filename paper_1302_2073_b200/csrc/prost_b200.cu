@@ -131,6 +131,17 @@ struct prost_handle {
   Args xa;
   prost_outputs xo{};
   bool xactive = false;
+  // in-kernel exchange over peer memory (prost_xpeer_handle / prost_xpeer_open):
+  // the frame runs as in single-GPU mode, the phase kernels exchange their sums
+  // through every rank's exchange region themselves
+  void* xp_region = nullptr;  // this rank's exchange region (cudaMalloc, exported by IPC)
+  int xp_world = 0;           // world size the region was sized for
+  std::vector<void*> xp_opened;  // peers' regions mapped through IPC
+  void** xp_table = nullptr;  // device [world]: every rank's region
+  unsigned long long* xseq = nullptr;  // device [S]
+  int xrank = 0, xworld = 0;
+  bool xpeer_on = false;
+  long long xframe = 0;
   // pipelined host I/O (prost_push with host frames and host outputs): upload
   // on s_in, kernels on s_comp, download on s_out, double-buffered, so the
   // copies of one frame overlap the kernels of the next
@@ -210,9 +221,22 @@ Args make_args(prost_handle* h, int s0) {
   const double p = h->prm.p;
   a.pmode = p == 2.0 ? PM_TWO : (p == 1.0 ? PM_ONE : ((p == 0.5 && !h->fp64) ? PM_HALF : PM_GENERAL));
   a.n_real = h->xmode ? h->n_real_glob : (long long)h->C * h->P;
-  if (h->xmode) {
+  if (h->xmode && !h->xpeer_on) {
     a.xred = h->xred;
     a.xgo = h->xgo;
+  }
+  if (h->xpeer_on) {
+    a.xpeer = h->xp_table;
+    a.xseq = h->xseq;
+    a.xrank = h->xrank;
+    a.xworld = h->xworld;
+    a.xS = h->S;
+    a.xhalo = (h->xrank > 0 ? 1 : 0) | (h->xrank < h->xworld - 1 ? 2 : 0);
+    a.xframe = h->xframe;
+    const int par = (int)(h->xframe & 1);
+    uint8_t* hb = static_cast<uint8_t*>(h->xp_region) + xr_halo_off(h->xworld, h->S, h->nvmax);
+    if (a.xhalo & 1) a.halo_top = hb + (size_t)(par * 2 + 0) * h->S * h->prm.width;
+    if (a.xhalo & 2) a.halo_bot = hb + (size_t)(par * 2 + 1) * h->S * h->prm.width;
   }
   a.p = p;
   a.half_p = 0.5 * p;
@@ -332,7 +356,10 @@ struct Impl {
       LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
       LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
     }
-    if (a.mask_out) LAUNCH(PROST_PH_MEDIAN, launch_median(h, a, st, sw));
+    if (a.mask_out) {
+      if (a.xpeer && a.xhalo) LAUNCH(PROST_PH_MEDIAN, (k_halo_push<<<dim3(1, sw), NT, 0, st>>>(a)));
+      LAUNCH(PROST_PH_MEDIAN, launch_median(h, a, st, sw));
+    }
     h->launches += n;
   }
 
@@ -352,6 +379,23 @@ struct Impl {
   static void step(prost_handle* h, Args& a, cudaStream_t st, int sw, int xs) {
     const dim3 grid(h->chunks, sw);
     long long n = 0;
+    if constexpr (std::is_same<T, float>::value && K > 20) {
+      if (h->tma && ((uintptr_t)a.x & 15) == 0 &&
+          (xs == XS_PASS0 || xs == XS_ITER || xs == XS_GRADFB || xs == XS_GEO)) {
+        Args at = a;
+        at.chunks = h->tma_chunks;
+        const dim3 tg(h->tma_chunks, sw);
+        constexpr size_t sm = tma_smem_small<K>(), sg = tma_smem_geo<K>();
+        switch (xs) {
+          case XS_PASS0: LAUNCH(PROST_PH_PASS0, (k_pass0_tma<K><<<tg, TT, sm, st>>>(at, h->umap))); break;
+          case XS_ITER: LAUNCH(PROST_PH_ITER, (k_iter_tma<K><<<tg, TT, sm, st>>>(at, h->umap))); break;
+          case XS_GRADFB: LAUNCH(PROST_PH_GRADFB, (k_gradfb_tma<K><<<tg, TT, sm, st>>>(at, h->umap))); break;
+          default: LAUNCH(PROST_PH_GEO, (k_geo_tma<K><<<tg, TT, sg, st>>>(at, h->umap))); break;
+        }
+        h->launches += n;
+        return;
+      }
+    }
     switch (xs) {
       case XS_STATS: LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a))); break;
       case XS_COLD: LAUNCH(PROST_PH_COLD, (k_cold<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
@@ -615,6 +659,7 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   }
   h->qr_due = h->qr_bound >= QR_EVERY - 1;
   h->qr_bound += 1;
+  if (h->xpeer_on) h->xframe += 1;
   const bool same = (dtype == PROST_F64) == h->fp64 && dtype != PROST_U8;
   const bool dense = h->P == h->Pp;
   const void* xdev = h->x;
@@ -1072,6 +1117,10 @@ void prost_destroy(prost_handle* h) {
                   h->rbar, h->rpart, h->rprof, h->xred, h->xgo, h->labc};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (void* pr : h->xp_opened) cudaIpcCloseMemHandle(pr);
+  if (h->xp_table) cudaFree(h->xp_table);
+  if (h->xseq) cudaFree(h->xseq);
+  if (h->xp_region) cudaFree(h->xp_region);
   // pipelined-I/O slot buffers (slot 0's frame buffer is h->x's allocation,
   // and h->x / bgbuf / resbuf / maskbuf may point at slot buffers)
   if (h->s_in) {
@@ -1406,7 +1455,8 @@ int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_
 int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_device,
                const prost_outputs* out, void* cuda_stream) {
   if (!h) return PROST_ERR_CONFIG;
-  if (h->xmode) return fail(h, PROST_ERR_CONFIG, "exchange-mode handle: use prost_xbegin");
+  if (h->xmode && !h->xpeer_on)
+    return fail(h, PROST_ERR_CONFIG, "exchange-mode handle: use prost_xbegin (or prost_xpeer_open)");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   Args a;
   prost_outputs o{};
@@ -1564,6 +1614,68 @@ int prost_xfinish(prost_handle* h, const uint8_t* halo_top, const uint8_t* halo_
   return push_outputs(h, a, h->xo, st);
 }
 
+// In-kernel exchange over peer memory.  Every rank allocates its exchange
+// region (prost_xpeer_handle), the caller all-gathers the IPC handles (64 bytes
+// each, any transport) and hands them to prost_xpeer_open; from then on
+// prost_push runs the whole frame on the device with the phase kernels'
+// cross-rank sums done in-kernel (xpeer_exchange) — only the phases that
+// actually run exchange, and no host round trip per phase.
+int prost_xpeer_handle(prost_handle* h, int32_t world, void* ipc_handle) {
+  if (!h || !ipc_handle) return PROST_ERR_CONFIG;
+  if (!h->xmode) return fail(h, PROST_ERR_CONFIG, "not an exchange-mode handle (prost_set_exchange)");
+  if (world < 1 || world > 64) return fail(h, PROST_ERR_CONFIG, "world size %d outside [1, 64]", world);
+  CK(cudaSetDevice(h->device));
+  if (h->xp_region && h->xp_world != world)
+    return fail(h, PROST_ERR_SEQUENCE, "exchange region already sized for %d ranks", h->xp_world);
+  if (!h->xp_region) {
+    const size_t bytes = xr_bytes(world, h->S, h->nvmax, h->prm.width);
+    CK(cudaMalloc(&h->xp_region, bytes));  // plain cudaMalloc: exportable through IPC
+    CK(cudaMemset(h->xp_region, 0, bytes));
+    h->xp_world = world;
+  }
+  cudaIpcMemHandle_t ih;
+  CK(cudaIpcGetMemHandle(&ih, h->xp_region));
+  static_assert(sizeof(cudaIpcMemHandle_t) == PROST_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(ipc_handle, &ih, sizeof ih);
+  return PROST_OK;
+}
+
+int prost_xpeer_open(prost_handle* h, int32_t rank, int32_t world, const void* ipc_handles) {
+  if (!h || !ipc_handles) return PROST_ERR_CONFIG;
+  if (!h->xp_region || h->xp_world != world)
+    return fail(h, PROST_ERR_SEQUENCE, "call prost_xpeer_handle with the same world size first");
+  if (rank < 0 || rank >= world) return fail(h, PROST_ERR_CONFIG, "rank %d outside world %d", rank, world);
+  if (h->xpeer_on) return fail(h, PROST_ERR_SEQUENCE, "peer exchange already open");
+  CK(cudaSetDevice(h->device));
+  std::vector<void*> bases(world, nullptr);
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) {
+      bases[q] = h->xp_region;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, static_cast<const uint8_t*>(ipc_handles) + (size_t)q * PROST_IPC_HANDLE_BYTES, sizeof ih);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (void* o : h->xp_opened) cudaIpcCloseMemHandle(o);
+      h->xp_opened.clear();
+      return fail(h, PROST_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+    }
+    h->xp_opened.push_back(p);
+    bases[q] = p;
+  }
+  CK(cudaMalloc(&h->xp_table, (size_t)world * sizeof(void*)));
+  CK(cudaMemcpy(h->xp_table, bases.data(), (size_t)world * sizeof(void*), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&h->xseq, (size_t)h->S * sizeof(unsigned long long)));
+  CK(cudaMemset(h->xseq, 0, (size_t)h->S * sizeof(unsigned long long)));
+  h->xrank = rank;
+  h->xworld = world;
+  h->xframe = 0;
+  h->xpeer_on = true;
+  return PROST_OK;
+}
+
 int prost_background(prost_handle* h, void* out, int32_t dtype, int32_t on_device, void* cuda_stream) {
   if (!h) return PROST_ERR_CONFIG;
   if (!out) return fail(h, PROST_ERR_DIMENSION, "out is NULL");
@@ -1700,6 +1812,15 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value) {
     case PROST_Q_TEAMS: *value = h->rT; break;
     case PROST_Q_GROUPS: *value = h->rng; break;
     case PROST_Q_QPC: *value = h->rqpc; break;
+    case PROST_Q_EXCHANGES: {  // in-kernel exchanges of stream 0 so far (synchronous read)
+      unsigned long long v = 0;
+      if (h->xseq) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(&v, h->xseq, sizeof v, cudaMemcpyDeviceToHost));
+      }
+      *value = (int64_t)v;
+      break;
+    }
     default: return fail(h, PROST_ERR_CONFIG, "unknown query %d", what);
   }
   return PROST_OK;

@@ -109,6 +109,15 @@ struct Args {
   int* xgo;            // [S]
   const uint8_t* halo_top;  // [S][width] label row above the local rows, or null
   const uint8_t* halo_bot;  // [S][width] label row below the local rows, or null
+  // In-kernel exchange over peer memory (pixel sharding after prost_xpeer_open;
+  // xred = null): the last CTA of a phase kernel stores the stream's sums into
+  // every rank's exchange region (NVLink peer stores), waits for every rank's
+  // flag and sums the ranks' vectors in rank order itself (xpeer_exchange).
+  void* const* xpeer;        // [xworld] exchange regions of all ranks (device table), or null
+  unsigned long long* xseq;  // [S] exchanges so far per stream (same on every rank)
+  int xrank, xworld, xS;     // this rank, ranks, streams of the handle
+  int xhalo;                 // bit 0: a rank above exists; bit 1: a rank below
+  long long xframe;          // frames pushed (label-row halo sequence)
   uint8_t* labc;       // [S][np] per-coordinate flags of the TMEM kernel (3 channels), or null
   int xu8;             // TMEM kernel: x holds 8-bit frames, divided by 255 on load (frameio.py:136)
   int nframes;         // TMEM kernel: consecutive frames per stream in this launch (frame blocking;
@@ -267,6 +276,96 @@ __device__ __forceinline__ double warp_sum(double x) {
 }
 
 // Reduce one per-thread value over the CTA into sm[warp][slot] (lane 0 writes).
+// ---------------------------------------------------------------------------
+// Exchange region of one rank (prost_xpeer_handle allocates it, peers write it):
+//   sums   [2 parity][world][S][nvmax] fp64   (parity = exchange sequence & 1)
+//   flags  [world][S] u64                     (last sequence number received)
+//   halos  [2 parity][2: row above, row below][S][width] u8
+//   hflags [2: above, below][S] u64           (last frame received)
+// Sequence numbers only grow, so flags need no parity; two data parities are
+// enough because a rank cannot start exchange n+2 before every rank has
+// contributed to n+1, i.e. finished reading n.
+__host__ __device__ inline size_t xr_sums_bytes(int world, int S, int nv) {
+  return (size_t)2 * world * S * nv * sizeof(double);
+}
+__host__ __device__ inline size_t xr_flags_off(int world, int S, int nv) { return xr_sums_bytes(world, S, nv); }
+__host__ __device__ inline size_t xr_halo_off(int world, int S, int nv) {
+  return (xr_flags_off(world, S, nv) + (size_t)world * S * 8 + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t xr_hflags_off(int world, int S, int nv, int width) {
+  return (xr_halo_off(world, S, nv) + (size_t)4 * S * width + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t xr_bytes(int world, int S, int nv, int width) {
+  return xr_hflags_off(world, S, nv, width) + (size_t)2 * S * 8;
+}
+__device__ __forceinline__ double* xr_sums(void* base, const Args& a, int par, int q, int s) {
+  return static_cast<double*>(base) + (((size_t)par * a.xworld + q) * a.xS + s) * a.nvmax;
+}
+__device__ __forceinline__ unsigned long long* xr_flag(void* base, const Args& a, int q, int s) {
+  return reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(base) + xr_flags_off(a.xworld, a.xS, a.nvmax)) +
+         (size_t)q * a.xS + s;
+}
+__device__ __forceinline__ uint8_t* xr_halo(void* base, const Args& a, int par, int which) {
+  return static_cast<uint8_t*>(base) + xr_halo_off(a.xworld, a.xS, a.nvmax) +
+         ((size_t)par * 2 + which) * a.xS * a.width;
+}
+__device__ __forceinline__ unsigned long long* xr_hflag(void* base, const Args& a, int which, int s) {
+  return reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(base) +
+                                               xr_hflags_off(a.xworld, a.xS, a.nvmax, a.width)) +
+         (size_t)which * a.xS + s;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= v; a rank that never arrives (a dead peer) traps after
+// ~10 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_flag(const unsigned long long* p, unsigned long long v) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) < v) {
+    __nanosleep(32);
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+}
+
+// The cross-rank sum of one phase, run by the last CTA of stream s: red[0..nv)
+// holds this rank's sums on entry and the all-rank sums, added in rank order,
+// on exit — the same numbers on every rank.
+template <int NTH>
+__device__ __noinline__ void xpeer_exchange(const Args& a, int s, int nv, double* red) {
+  __shared__ unsigned long long sseq;
+  if (threadIdx.x == 0) {
+    sseq = a.xseq[s] + 1;
+    a.xseq[s] = sseq;
+  }
+  __syncthreads();
+  const unsigned long long seq = sseq;
+  const int par = (int)(seq & 1ull);
+  for (int i = threadIdx.x; i < a.xworld * nv; i += NTH) {
+    const int q = i / nv, v = i - q * nv;
+    xr_sums(a.xpeer[q], a, par, a.xrank, s)[v] = red[v];  // peer store (NVLink)
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < a.xworld) {
+    __threadfence_system();
+    st_release_sys(xr_flag(a.xpeer[threadIdx.x], a, a.xrank, s), seq);
+    wait_flag(xr_flag(a.xpeer[a.xrank], a, threadIdx.x, s), seq);
+  }
+  __syncthreads();
+  void* own = a.xpeer[a.xrank];
+  for (int v = threadIdx.x; v < nv; v += NTH) {
+    double acc = 0.0;
+    for (int q = 0; q < a.xworld; ++q) acc += __ldcv(xr_sums(own, a, par, q, s) + v);
+    red[v] = acc;
+  }
+  __syncthreads();
+}
+
 // NTH: threads of the CTA (the TMA-fed streamed kernels run 512).
 template <int NTH = NT>
 __device__ __forceinline__ void cta_stage(double x, double* sm, int slot, int nv) {
@@ -327,6 +426,7 @@ __device__ __forceinline__ bool cta_finish(const Args& a, int s, double* sm, int
     }
     __syncthreads();
   }
+  if (a.xpeer) xpeer_exchange<NTH>(a, s, nv, red);
   return a.xred == nullptr;
 }
 

@@ -791,11 +791,46 @@ __global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// Label-row halos over peer memory (pixel sharding, prost_xpeer_open): this
+// rank's first label row goes to the rank above (its row below), its last row
+// to the rank below (its row above); the flag carries the frame number.
+static __global__ void __launch_bounds__(NT) k_halo_push(const __grid_constant__ Args a) {
+  const int s = a.s0 + blockIdx.y;
+  const int W = a.width, H = a.height, par = (int)(a.xframe & 1);
+  const uint8_t* L = a.lab + (size_t)s * a.Pp;
+  uint8_t* up = (a.xhalo & 1) ? xr_halo(a.xpeer[a.xrank - 1], a, par, 1) + (size_t)s * W : nullptr;
+  uint8_t* dn = (a.xhalo & 2) ? xr_halo(a.xpeer[a.xrank + 1], a, par, 0) + (size_t)s * W : nullptr;
+  for (int x = threadIdx.x; x < W; x += NT) {
+    if (up) up[x] = L[x];
+    if (dn) dn[x] = L[(size_t)(H - 1) * W + x];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (up) st_release_sys(xr_hflag(a.xpeer[a.xrank - 1], a, 1, s), (unsigned long long)a.xframe);
+    if (dn) st_release_sys(xr_hflag(a.xpeer[a.xrank + 1], a, 0, s), (unsigned long long)a.xframe);
+  }
+}
+
+// The median's wait for this frame's halo rows from the neighbouring ranks.
+__device__ __forceinline__ void halo_wait(const Args& a, int s) {
+  if (!a.xpeer) return;
+  if (threadIdx.x == 0) {
+    void* own = a.xpeer[a.xrank];
+    if (a.xhalo & 1) wait_flag(xr_hflag(own, a, 0, s), (unsigned long long)a.xframe);
+    if (a.xhalo & 2) wait_flag(xr_hflag(own, a, 1, s), (unsigned long long)a.xframe);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // k_median: 3x3 majority vote with edge replication (pipeline.py:215-228).
 
 static __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
+  halo_wait(a, s);
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
   uint8_t* M = a.mask_out + (size_t)s * a.Pp;
   const int W = a.width, H = a.height;
@@ -826,6 +861,7 @@ static __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Ar
 static __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
+  halo_wait(a, s);
   const int W = a.width, H = a.height, wq = W >> 2;
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
   uint32_t* M = reinterpret_cast<uint32_t*>(a.mask_out + (size_t)s * a.Pp);
@@ -855,6 +891,7 @@ static __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ A
 static __global__ void __launch_bounds__(NT) k_median16(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
+  halo_wait(a, s);
   const int W = a.width, H = a.height, wq = W >> 4;
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
   uint8_t* M = a.mask_out + (size_t)s * a.Pp;

@@ -12,6 +12,18 @@ scalar logic, so the row blocks stay one basis.  The 3x3 median takes the
 label row above and below each block from the neighbouring ranks.  No other
 data crosses ranks.
 
+Two ways to run the exchange (`exchange=`):
+  "program"  the host drives it: after each phase kernel it all-reduces the
+             exchange buffer (NCCL on the kernels' stream, gloo through the
+             host) and applies the phase's logic (prost_xnext / xapply) —
+             every phase that *can* run exchanges, 7 per frame at C4;
+  "peer"     the kernels do it (prost_xpeer_open): the last CTA of each phase
+             kernel stores the stream's sums into every rank's exchange region
+             over NVLink and sums all ranks' vectors itself, so a frame is one
+             prost_push, only the phases that run exchange (3 per steady-state
+             frame at C4), and the median's halo rows arrive by peer stores.
+             Needs CUDA IPC between the ranks' devices (one node).
+
 The reference has no multi-device path; this class is the same
 `StreamTracker.push` seam (jobs.py:186-229) for one stream whose frame and
 outputs are each rank's row block.
@@ -61,7 +73,7 @@ class ShardedTracker:
 
     def __init__(self, config: RunConfig, group=None, i_init: Optional[int] = None, *,
                  precision: str = "fp32", device: int = 0, seed: Optional[int] = None,
-                 basis: Optional[np.ndarray] = None):
+                 basis: Optional[np.ndarray] = None, exchange: str = "program"):
         import torch
         import torch.distributed as dist
 
@@ -96,6 +108,16 @@ class ShardedTracker:
         self.gathered = torch.zeros((self.world, 2, W), dtype=torch.uint8, device=f"cuda:{device}")
         self.exchanges = 0  # cross-rank all-reduces issued (the exchange program)
         self.frames = 0
+        if exchange not in ("program", "peer"):
+            raise ConfigError(f"exchange must be 'program' or 'peer', got {exchange!r}")
+        self.exchange = exchange
+        if exchange == "peer":
+            handle = self.native.xpeer_handle(self.world)
+            handles = [handle]
+            if self.world > 1:
+                handles = [None] * self.world
+                dist.all_gather_object(handles, handle, group=group)
+            self.native.xpeer_open(self.rank, self.world, handles)
 
     # -- layout ---------------------------------------------------------------
     def local_rows(self, full):
@@ -147,6 +169,10 @@ class ShardedTracker:
              fit: bool = False, cuda_stream: int = 0):
         """One frame: every rank calls push with its row block at the same time."""
         nt = self.native
+        if self.exchange == "peer":
+            self.frames += 1
+            return nt.push(block, background=background, residual=residual, mask=mask,
+                           raw_mask=raw_mask, fit=fit, cuda_stream=cuda_stream)
         nt.xbegin(block, background=background, residual=residual, mask=mask, raw_mask=raw_mask,
                   fit=fit, cuda_stream=cuda_stream)
         self.frames += 1
@@ -165,6 +191,11 @@ class ShardedTracker:
             if self.rank < self.world - 1:
                 halo_bot = self.gathered[self.rank + 1, 0].data_ptr()
         return nt.xfinish(halo_top, halo_bot, cuda_stream)
+
+    def peer_exchanges(self) -> int:
+        """In-kernel exchanges so far (peer mode; synchronizes the device)."""
+        from . import _native as nat
+        return self.native.query(nat.Q_EXCHANGES)
 
     def get_basis_block(self) -> np.ndarray:
         return self.native.get_core_state(0)[0]

@@ -405,6 +405,21 @@ class NativeTracker:
         self._check(self._lib.prost_xedges(self._h, ctypes.c_void_p(top), ctypes.c_void_p(bottom),
                                            ctypes.c_void_p(cuda_stream)), "xedges")
 
+    def xpeer_handle(self, world: int) -> bytes:
+        """IPC handle (64 bytes) of this rank's exchange region, sized for `world` ranks."""
+        buf = ctypes.create_string_buffer(nat.IPC_HANDLE_BYTES)
+        self._check(self._lib.prost_xpeer_handle(self._h, int(world), buf), "xpeer_handle")
+        return buf.raw
+
+    def xpeer_open(self, rank: int, world: int, handles) -> None:
+        """Map every rank's exchange region (`handles`: the world's IPC handles in
+        rank order); prost_push then runs the frame with in-kernel exchanges."""
+        blob = b"".join(bytes(hd) for hd in handles)
+        if len(blob) != world * nat.IPC_HANDLE_BYTES:
+            raise DimensionError(f"{len(blob)} handle bytes for {world} ranks")
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        self._check(self._lib.prost_xpeer_open(self._h, int(rank), int(world), buf), "xpeer_open")
+
     def xfinish(self, halo_top=None, halo_bottom=None, cuda_stream: int = 0):
         self._check(self._lib.prost_xfinish(self._h, ctypes.c_void_p(halo_top),
                                             ctypes.c_void_p(halo_bottom),

@@ -196,10 +196,12 @@ def test_c4_row_block_teacher_forced():
     assert_tf(teacher_forced(run, 36))
 
 
-def test_c4_row_block_exchange_program_teacher_forced():
-    """The pixel-sharded exchange program (ShardedTracker at world size 1:
-    every phase's partials go through the exchange buffer and k_xlogic)
-    against the oracle on the same 3840x48 k=30 block."""
+@pytest.mark.parametrize("exchange", ["program", "peer"])
+def test_c4_row_block_exchange_program_teacher_forced(exchange):
+    """The pixel-sharded exchange (ShardedTracker at world size 1) against the
+    oracle on the same 3840x48 k=30 block: "program" — every phase's partials
+    go through the exchange buffer and k_xlogic; "peer" — the phase kernels
+    exchange through the peer-memory region themselves."""
     import torch
 
     from oracle import prost_oracle as orc
@@ -209,7 +211,7 @@ def test_c4_row_block_exchange_program_teacher_forced():
 
     cfg = pkg.RunConfig(i_init=20, **dict(CONFIGS["C4"]["tracker"], target_height=48))
     frames = config_frames("C4", 0, 36, height=48)
-    st = ShardedTracker(cfg)
+    st = ShardedTracker(cfg, exchange=exchange)
     o = oracle_for(cfg, 20, 3840, 48, 1, 0)
     P = 3840 * 48
     bg = torch.empty(P, dtype=torch.float32, device="cuda")
@@ -231,6 +233,10 @@ def test_c4_row_block_exchange_program_teacher_forced():
               (info.iterations, info.cost_evals) == (r.fit.iterations, r.fit.cost_evals),
               r.fit.armijo_margin)
     assert_tf(w)
+    if exchange == "peer":
+        # only the phases that ran exchanged: statistics in the window, pass 0,
+        # the CG iterations, rare fallbacks — never the program's 7+ per frame
+        assert 36 * 2 <= st.peer_exchanges() <= 36 * 5
 
 
 def test_u8_frames_against_oracle():

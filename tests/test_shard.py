@@ -62,11 +62,11 @@ def _unsharded(frames):
     return np.array(masks), np.array(bgs), bt.native.get_core_state(0)[0]
 
 
-def _sharded_run(frames, group=None):
+def _sharded_run(frames, group=None, exchange="program"):
     import torch
     from paper_1302_2073_b200.shard import ShardedTracker
 
-    st = ShardedTracker(_cfg(), group=group)
+    st = ShardedTracker(_cfg(), group=group, exchange=exchange)
     n = st.rows * W
     mask = torch.empty(n, dtype=torch.uint8, device="cuda")
     bg = torch.empty(n, dtype=torch.float32, device="cuda")
@@ -87,6 +87,23 @@ def test_world1_matches_unsharded_bitwise():
     np.testing.assert_array_equal(m1, m0)
     np.testing.assert_array_equal(b1, b0)
     np.testing.assert_array_equal(U1, U0)
+
+
+@pytest.mark.gpu
+def test_peer_exchange_world1_matches_unsharded_bitwise():
+    """In-kernel exchange through the peer-memory region (world size 1: the
+    region is this rank's own): the same results bit for bit, and only the
+    phases that ran exchanged."""
+    frames = _frames()
+    m0, b0, U0 = _unsharded(frames)
+    m1, b1, U1, st = _sharded_run(frames, exchange="peer")
+    np.testing.assert_array_equal(m1, m0)
+    np.testing.assert_array_equal(b1, b0)
+    np.testing.assert_array_equal(U1, U0)
+    _, _, _, sp = _sharded_run(frames)
+    ex = st.peer_exchanges()
+    assert F <= ex < sp.exchanges
+    assert st.native.query(0) < sp.native.query(0)  # fewer launches: no k_xlogic
 
 
 def _worker(rank, world, port, frames, out):
