@@ -216,10 +216,27 @@ def reference_kind():
     return "reference" if (REF_DIR / "prost" / "jobs.py").exists() else "port"
 
 
+def cpu_plan(tracker, n_frames, cores, preroll=100):
+    """Bound the CPU sample: the reference costs ~4.5e-8 s per coordinate x k
+    per frame on one core (11 s per C4 frame) and holds
+    a few fp64 copies of the n x k basis, so very large streams (C4) run on
+    fewer workers, pre-roll 1 frame instead of the statistics window and time
+    2 frames; the sample text says so."""
+    n = tracker["target_width"] * tracker["target_height"] * (1 if tracker["grayscale"] else 3)
+    k = tracker["subspace_dim"]
+    t_frame = 4.5e-8 * n * k
+    cores = max(1, min(cores, int(24e9 // (n * k * 32))))
+    if (preroll + n_frames) * t_frame > 60.0:
+        preroll = 1
+        n_frames = max(2, min(n_frames, int(30.0 / t_frame)))
+    return n_frames, cores, preroll
+
+
 def cpu_rate(name, tracker, n_frames, cores=None, kind=None, preroll=100):
     import multiprocessing as mp
 
     cores = cores or len(os.sched_getaffinity(0))
+    n_frames, cores, preroll = cpu_plan(tracker, n_frames, cores, preroll)
     kind = kind or reference_kind()
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ctx = mp.get_context("spawn")
@@ -230,7 +247,15 @@ def cpu_rate(name, tracker, n_frames, cores=None, kind=None, preroll=100):
     wall = time.perf_counter() - t0
     frames = sum(r[0] for r in res)
     slowest = max(r[1] for r in res)
+    cpu_rate.last_preroll = preroll
     return frames / slowest, cores, frames, wall, kind
+
+
+def _window_note(name):
+    pre = getattr(cpu_rate, "last_preroll", 100)
+    return (f"{name} stream after the 100-frame statistics window" if pre >= 100 else
+            f"{name} stream after a {pre}-frame pre-roll (bounded sample: the full statistics "
+            "window would take minutes per worker at this size)")
 
 
 def cpu_model():
@@ -282,6 +307,7 @@ def run_reference(args):
     # the GPU arm's steady-state window (the statistics window is pre-rolled)
     n_frames = args.warmup + args.steps
     rate, cores, frames, wall, kind = cpu_rate(args.config, tracker, n_frames, cores)
+    n_frames = frames // cores
     W, H = tracker["target_width"], tracker["target_height"]
     P = W * H
     line = {
@@ -296,7 +322,7 @@ def run_reference(args):
         "cpu_baseline": {"value": rate, "unit": "stream-frames/s", "cores": cores,
                          "kind": kind, "cpu": cpu_model(),
                          "sample": f"{cores} worker processes x {n_frames} frames of their own "
-                                   f"{args.config} stream after the 100-frame statistics window "
+                                   f"{_window_note(args.config)} "
                                    f"({'the reference package prost.jobs.StreamTracker.push' if kind == 'reference' else 'numpy port of the reference path'}, "
                                    "OPENBLAS_NUM_THREADS=1)"},
         "e2e": {"value": rate, "unit": "stream-frames/s", "h2d_bytes_per_step": 0,
@@ -602,8 +628,8 @@ def main():
             rate, cores, frames, wall, kind = cpu_rate(args.config, tracker, args.cpu_frames)
             cpu = {"value": rate, "unit": "stream-frames/s", "cores": cores, "kind": kind,
                    "cpu": cpu_model(),
-                   "sample": f"{cores} worker processes x {args.cpu_frames} frames of their own "
-                             f"{args.config} stream after the 100-frame statistics window "
+                   "sample": f"{cores} worker processes x {frames // cores} frames of their own "
+                             f"{_window_note(args.config)} "
                              f"({'prost.jobs.StreamTracker.push, the reference package' if kind == 'reference' else 'numpy port of the reference path'}, "
                              f"OPENBLAS_NUM_THREADS=1; {wall:.1f} s wall)"}
             if kind == "reference" and args.cpu_port:

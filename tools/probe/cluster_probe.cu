@@ -42,7 +42,7 @@ int main() {
   const size_t smem = 200 * 1024;
   cudaFuncSetAttribute(kprobe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kprobe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  for (int cs : {2, 4, 8, 16}) {
+  for (int cs : {2, 4, 8, 9, 10, 11, 12, 13, 14, 16}) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs * 8);
     cfg.blockDim = dim3(512);
