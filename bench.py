@@ -342,8 +342,17 @@ def main():
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PROST_BENCH_SHARE_GPU") == "1":
+            # test of the multi-rank code path on a box with fewer GPUs than
+            # ranks: ranks share devices (their kernels never wait on each
+            # other — stream sharding has no data-path collective), gloo for
+            # the timing reductions (NCCL refuses two ranks on one device)
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
