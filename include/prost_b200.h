@@ -179,6 +179,8 @@ int prost_last_error(prost_handle* h, char* buf, int32_t len);
 #define PROST_Q_GROUPS 8     /* slot groups per CTA of the TMEM kernel: streams per team in flight */
 #define PROST_Q_QPC 9        /* row groups (4 coordinates) per CTA slice (resident modes) */
 #define PROST_Q_EXCHANGES 10 /* in-kernel cross-rank exchanges of stream 0 so far (peer mode) */
+#define PROST_Q_CLUSTER 11   /* 1: TMEM kernel teams run as thread-block clusters (DSMEM team sums) */
+#define PROST_Q_TMA 12       /* CTAs per stream of the TMA-fed streamed kernels (k > 20), 0: not used */
 int prost_query(prost_handle* h, int32_t what, int64_t* value);
 
 /* Per-phase device timing (CUDA events around every launch, on the launch

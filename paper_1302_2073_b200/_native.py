@@ -22,7 +22,7 @@ F32, F64, U8 = 0, 1, 2
 FLAG_PIPELINE, FLAG_FP64, FLAG_LATENCY = 1, 2, 4
 Q_LAUNCHES, Q_WAVE, Q_BYTES_U, Q_CHUNKS, Q_INSTANCE_K = 0, 1, 2, 3, 4
 Q_RESIDENT, Q_TEAM, Q_TEAMS, Q_GROUPS, Q_QPC = 5, 6, 7, 8, 9
-Q_EXCHANGES = 10
+Q_EXCHANGES, Q_CLUSTER, Q_TMA = 10, 11, 12
 IPC_HANDLE_BYTES = 64
 
 EXPORTS = (

@@ -13,7 +13,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 # translation units, compiled in parallel and linked into one library
-SRCS = [PKG / "csrc" / n for n in ("prost_b200.cu", "tmem_k.cu", "tmem_blk_k.cu", "resident_k.cu")]
+SRCS = [PKG / "csrc" / n for n in ("prost_b200.cu", "tmem_k.cu", "tmem_blk_k.cu", "tmem_cl_k.cu", "resident_k.cu")]
 DEPS = sorted((PKG / "csrc").glob("*.cu*")) + sorted((ROOT / "include").glob("*.h")) + [
     Path(__file__).resolve()]
 OUT = PKG / "_lib" / "libprost_b200.so"

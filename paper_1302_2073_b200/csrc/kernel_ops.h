@@ -35,7 +35,9 @@ struct TmOps {
   int qt;  // row groups per thread held in TMEM
   int ng;  // slot groups per CTA
   void (*describe)();
+  int (*clusters)(size_t smem, int cluster);  // cluster instances: clusters that fit the chip at once
 };
-TmOps pick_tmem(int K, bool half, int ng, bool blk = false);
+// blk: the frame-blocking instance; cl: one thread-block cluster per team
+TmOps pick_tmem(int K, bool half, int ng, bool blk = false, bool cl = false);
 
 }  // namespace prost_ops

@@ -61,6 +61,7 @@ struct prost_handle {
   bool tmem = false;
   int rG = 0, rT = 0, rqpc = 0, rnt = 0;
   int rng = 1;  // k_tmem slot groups per CTA
+  bool tm_cl = false;  // k_tmem teams as thread-block clusters (team sums over DSMEM)
   size_t rsmem = 0;
   unsigned* rbar = nullptr;
   double* rpart = nullptr;
@@ -782,12 +783,12 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
              h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0,
              alt ? atoi(alt) : 1};
-    CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
+    if (!h->tm_cl) CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
     long long n = 0;
     {
       PhaseTimer pt_(h, st, PROST_PH_FRAME);
       if (h->tmem)
-        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng).launch(a, ra, h->rsmem, st));
+        CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng, false, h->tm_cl).launch(a, ra, h->rsmem, st));
       else
         CK(pick_resident(h->resident_ops_K, h->prm.p == 0.5).launch(a, ra, h->rnt, h->rsmem, st));
       ++n;
@@ -1045,8 +1046,20 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
         ALLOC(rbar, (size_t)sms * TM_CPS * 2 * sizeof(unsigned));
         ALLOC(rpart, (size_t)2 * sms * TM_CPS * 2 * RES_RNV_MAX * sizeof(double));
         ALLOC(rprof, (size_t)sms * TM_CPS * PROF_N * sizeof(unsigned long long));
+        // A team that fits one thread-block cluster (<= 16 CTAs), with every
+        // team's cluster resident at once (the one-stream latency layout: C0),
+        // sums over DSMEM with the hardware cluster barrier instead of global
+        // slots and a counter barrier.  (C3's 13-CTA teams: only 7 such
+        // clusters fit the chip, against 11 teams of plain CTAs.)
+        const char* clenv = getenv("PROST_CLUSTER");
+        if (G <= 16 && !(clenv && clenv[0] == '0')) {
+          const TmOps tc = pick_tmem(K, params->p == 0.5, ng, false, true);
+          if (tc.launch && tc.prepare(sm) == cudaSuccess && tc.clusters(sm, G) >= h->rT) h->tm_cl = true;
+          cudaGetLastError();
+        }
         if (getenv("PROST_DEBUG"))
-          fprintf(stderr, "prost: tmem NG=%d G=%d T=%d qpc=%d smem=%zu\n", ng, G, h->rT, qpc, sm);
+          fprintf(stderr, "prost: tmem NG=%d G=%d T=%d qpc=%d smem=%zu cluster=%d\n", ng, G, h->rT, qpc, sm,
+                  (int)h->tm_cl);
       }
       cudaGetLastError();
       break;
@@ -1808,6 +1821,8 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value) {
     case PROST_Q_CHUNKS: *value = h->chunks; break;
     case PROST_Q_INSTANCE_K: *value = h->ops.K; break;
     case PROST_Q_RESIDENT: *value = h->tmem ? 2 : (h->resident ? 1 : 0); break;
+    case PROST_Q_CLUSTER: *value = h->tm_cl ? 1 : 0; break;
+    case PROST_Q_TMA: *value = h->tma ? h->tma_chunks : 0; break;
     case PROST_Q_TEAM: *value = h->rG; break;
     case PROST_Q_TEAMS: *value = h->rT; break;
     case PROST_Q_GROUPS: *value = h->rng; break;

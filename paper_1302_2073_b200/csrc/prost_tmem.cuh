@@ -115,11 +115,66 @@ __device__ __forceinline__ void group_sync(int g) {
 // team_sum / rstage / stage_floats of one slot group: wred is the group's
 // [TG/32][nv] staging, lt the thread within the group; the team's slots and
 // barrier counter are those of virtual team vt.
-template <int NG>
+// CL: the team is one thread-block cluster (one CTA per rank): the CTA sums
+// stay in each CTA's shared memory, the hardware cluster barrier replaces the
+// counter barrier, and every CTA reads its peers' sums over DSMEM — added in
+// the same order as the global-slot path (lane = rank, then the warp
+// butterfly), so both give the same bits.
+constexpr int CL_NV = 64;
+template <int NG, bool CL = false>
 __device__ __forceinline__ void team_sum_g(const RArgs& ra, int vt, int VT, int rank, int g, int lt,
                                            const double* wred, int nv, double* red, unsigned& epoch,
                                            unsigned long long* sprof) {
   constexpr int TG = TM_NT / NG, NWG = TG / 32;
+  if constexpr (CL) {
+    static_assert(NG == 1, "cluster team sums: one slot group");
+    __shared__ double cpart[2][CL_NV];
+    __syncthreads();
+    const bool tp = ra.prof && lt == 0;
+    const unsigned long long t0 = tp ? ptimer() : 0;
+    const int warp = lt >> 5, lane = lt & 31;
+    const int par = epoch & 1;
+    ++epoch;
+    for (int v = lt; v < nv; v += TG) {
+      double acc = 0.0;
+      for (int w = 0; w < NWG; ++w) acc += wred[w * nv + v];
+      cpart[par][v] = acc;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const unsigned long long t1 = tp ? ptimer() : 0;
+    // every load in flight at once (nv <= 4 * NWG), then the butterflies
+    for (int v0 = warp; v0 < nv; v0 += 4 * NWG) {
+      double x[4];
+      bool have[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int v = v0 + i * NWG;
+        have[i] = v < nv && lane < ra.G;
+        x[i] = 0.0;
+        if (have[i]) {
+          unsigned remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_addr(&cpart[par][v])), "r"(lane));
+          asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(x[i]) : "r"(remote) : "memory");
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double acc = 0.0;
+        if (have[i]) acc += x[i];
+        const double t = warp_sum(acc);
+        const int v = v0 + i * NWG;
+        if (lane == 0 && v < nv) red[v] = t;
+      }
+    }
+    __syncthreads();
+    if (tp) {
+      const unsigned long long t2 = ptimer();
+      sprof[PROF_BARRIER] += t1 - t0;
+      sprof[PROF_SLOTS] += t2 - t1;
+      sprof[PROF_NSUMS] += 1;
+    }
+    return;
+  }
   group_sync<NG>(g);
   const bool tp = ra.prof && g == 0 && lt == 0;
   unsigned long long t0 = tp ? ptimer() : 0;
@@ -296,7 +351,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 // the groups' slice loads alternate A, B, A, B, ...).
 // BLK: the frame-blocking instance (prost_push_many); the single-frame
 // instance compiles the blocking paths out (they cost registers).
-template <int K, int PM, int NG, bool BLK>
+template <int K, int PM, int NG, bool BLK, bool CL = false>
 __global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
@@ -516,7 +571,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       rstage_g(s1, wred, 0, 3, lt);
       rstage_g(s2, wred, 1, 3, lt);
       rstage_g(nf, wred, 2, 3, lt);
-      team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, 3, red, epoch, sprof);
+      team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, 3, red, epoch, sprof);
       if (lt == 0) {
         if (red[2] > 0.0) {
           cs->status = ST_NONFINITE;
@@ -686,7 +741,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         mean_pending = false;
         stage_floats_g<K>(pkc, wred, K + 1, 0, lt);
         rstage_g(bad ? 1.0 : 0.0, wred, K, K + 1, lt);
-        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
+        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
         if (lt < 32) {
           if (red[K] > 0.0) mark_nonfinite(cs, a, s, lt);
           else if (lt < k) cs->y[lt] = red[lt];
@@ -726,7 +781,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         rstage_g(cost, wred, 0, K + 3, lt);
         stage_floats_g<K + 1>(pk, wred, K + 3, 1, lt);
         rstage_g(bad ? 1.0 : 0.0, wred, K + 2, K + 3, lt);
-        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, K + 3, red, epoch, sprof);
+        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, K + 3, red, epoch, sprof);
         LOGIC(TM_AFTER_PASS0<K>(cs, a, s, lt, red));
         group_sync<NG>(g);
       }
@@ -774,7 +829,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         });
 #pragma unroll
         for (int m = 0; m < LSW; ++m) rstage_g((double)cst[m], wred, m, LSW, lt);
-        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, LSW, red, epoch, sprof);
+        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, LSW, red, epoch, sprof);
         LOGIC(TM_AFTER_LSFB(cs, a, s, lt, red, base));
       } else if (cs->need_gradfb) {
         const float al = (float)cs->acc_alpha;
@@ -799,7 +854,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
         });
         stage_floats_g<K + 1>(pk, wred, K + 1, 0, lt);
-        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
+        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
         LOGIC(TM_AFTER_GRADFB<K>(cs, a, s, lt, red));
       } else {
         constexpr int NV = WC + WG * (K + 1);
@@ -891,7 +946,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
             sprof[PROF_SW_ALL] += ptimer() - tsw0;
           }
         }
-        team_sum_g<NG>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
+        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
         {
           const unsigned long long tli = (ra.prof && tid == 0) ? ptimer() : 0;
           LOGIC(TM_AFTER_ITER<K>(cs, a, s, lt, red, wlo));
@@ -1061,6 +1116,8 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   }
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tbase), "n"(TM_NT));
+  if constexpr (CL)  // no CTA leaves while a peer may still read its team sums
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace prost
