@@ -784,6 +784,11 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
              h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0,
              alt ? atoi(alt) : 1};
     if (!h->tm_cl) CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
+    // cluster teams filter the labels themselves (one channel, 4-pixel words)
+    // (not when the periodic QR may run after the kernel: it relabels)
+    const bool med_in =
+        h->tm_cl && h->C == 1 && h->prm.width % 4 == 0 && h->P == h->Pp && a.mask_out && !h->qr_due;
+    ra.median = med_in ? 1 : 0;
     long long n = 0;
     {
       PhaseTimer pt_(h, st, PROST_PH_FRAME);
@@ -799,7 +804,7 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
       ++n;
     }
     if (h->tmem && h->qr_due) h->ops.qr(h, a, st, h->S);  // per stream: exits unless due
-    if (a.mask_out) {
+    if (a.mask_out && !med_in) {
       PhaseTimer pt_(h, st, PROST_PH_MEDIAN);
       launch_median(h, a, st, h->S);
       ++n;

@@ -34,6 +34,7 @@ struct RArgs {
   int stagger_ns;            // start delay of odd teams (k_tmem), 0 = none
   int prefetch;              // k_tmem: L2 prefetch of the next stream's slice
   int alt;                   // k_tmem with 2 slot groups: alternate the groups' slice loads
+  int median;                // k_tmem cluster teams: the 3x3 label median in-kernel (mask_out)
 };
 
 // Timing counters of one CTA (thread 0, %globaltimer ns): see PROF_* below.

@@ -1103,6 +1103,41 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     if (rank == 0 && lt < (int)(sizeof(Ctl) / 8))
       reinterpret_cast<double*>(a.ctl + s)[lt] = reinterpret_cast<const double*>(cs)[lt];
     group_sync<NG>(g);
+
+    // ---- cluster teams: the stream's 3x3 label median here (pipeline.py:
+    // 215-228, edge replication) instead of in a separate kernel — after the
+    // cluster barrier every label of the team's stream is written; L2 reads
+    // (__ldcg), since other CTAs wrote them during this launch
+    if constexpr (CL && !BLK) {
+      if (ra.median) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (cs->status == ST_OK) {
+          const int W = a.width, H = a.height, wq = W >> 2;
+          const uint8_t* L = a.lab + (size_t)s * a.Pp;
+          uint32_t* M = reinterpret_cast<uint32_t*>(a.mask_out + (size_t)s * a.Pp);
+          for (int qi = lt; qi < qcount; qi += TG) {
+            const int q = q0 + qi;
+            if (q * 4 >= a.P) continue;
+            const int yy = q / wq, x0 = (q - yy * wq) << 2;
+            const int xl = x0 > 0 ? x0 - 1 : 0, xr = x0 + 4 < W ? x0 + 4 : W - 1;
+            const uint8_t* ra_ = L + (size_t)(yy > 0 ? yy - 1 : 0) * W;
+            const uint8_t* rm = L + (size_t)yy * W;
+            const uint8_t* rb = L + (size_t)(yy < H - 1 ? yy + 1 : H - 1) * W;
+            const uint32_t v = __ldcg(reinterpret_cast<const unsigned*>(ra_ + x0)) +
+                               __ldcg(reinterpret_cast<const unsigned*>(rm + x0)) +
+                               __ldcg(reinterpret_cast<const unsigned*>(rb + x0));
+            const uint32_t l = (uint32_t)__ldcg(reinterpret_cast<const unsigned char*>(ra_ + xl)) +
+                               __ldcg(reinterpret_cast<const unsigned char*>(rm + xl)) +
+                               __ldcg(reinterpret_cast<const unsigned char*>(rb + xl));
+            const uint32_t r = (uint32_t)__ldcg(reinterpret_cast<const unsigned char*>(ra_ + xr)) +
+                               __ldcg(reinterpret_cast<const unsigned char*>(rm + xr)) +
+                               __ldcg(reinterpret_cast<const unsigned char*>(rb + xr));
+            const uint32_t win = v + ((v << 8) | l) + ((v >> 8) | (r << 24));
+            M[q] = __vcmpgeu4(win, 0x05050505u) & 0x01010101u;
+          }
+        }
+      }
+    }
   }
   if (NG > 1 && lt == 0) s_done[g] = 1;
 #undef LOGIC

@@ -294,6 +294,40 @@ def test_batched_streams_bitwise_match_single_streams():
         np.testing.assert_array_equal(Ub, U1)
 
 
+def test_cluster_team_sums_match_global_slots(monkeypatch):
+    """Teams run as thread-block clusters (team sums over DSMEM with the
+    hardware cluster barrier) give the same bits as the global-slot team sums
+    (C0 shape, one-stream latency layout: G = 10 fits one cluster)."""
+    import torch
+    from paper_1302_2073_b200 import _native as nat
+
+    W, H, F = 160, 120, 12
+    frames = c0_stream(F)
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=4, seed=0)
+
+    def run():
+        bt = pkg.BatchTracker(cfg, 1, seeds=[0], latency=True)
+        mask = torch.empty((1, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((1, W * H), dtype=torch.float32, device="cuda")
+        out = []
+        for f in range(F):
+            info = bt.push(torch.from_numpy(frames[f][None].astype(np.float32)).cuda(), background=bg,
+                           mask=mask, fit=True)
+            out.append((mask.cpu().numpy().copy(), bg.cpu().numpy().copy(), info[0].fit_cost))
+        return out, bt.native.get_core_state(0)[0], bt.native.query(nat.Q_CLUSTER)
+
+    a, Ua, cla = run()
+    monkeypatch.setenv("PROST_CLUSTER", "0")
+    b, Ub, clb = run()
+    assert (cla, clb) == (1, 0)
+    for (ma, ba, ca), (mb, bb, cb) in zip(a, b):
+        np.testing.assert_array_equal(ma, mb)
+        np.testing.assert_array_equal(ba, bb)
+        assert ca == cb
+    np.testing.assert_array_equal(Ua, Ub)
+
+
 def test_large_batch_properties():
     """C3 shape (320x240, k=15) with 8 streams for 6 frames: size-independent
     properties — orthonormality, raw mask == threshold of the residual, mask ==
