@@ -526,11 +526,25 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms_b = max_over_ranks(e0.elapsed_time(e1)) / (reps * FB)
+        # per-phase split of one blocked call (separate, untimed)
+        native.profile(True)
+        bt.push_many(frames_dev[step:step + FB], background=bg_b, mask=mask_b)
+        step += FB
+        torch.cuda.synchronize()
+        ph_b = native.profile_read()
+        native.profile(False)
+        tmem_blk = native.query(nat.Q_RESIDENT) == 2
         blocked = {"frames_per_call": FB, "value": units / (ms_b / 1000.0), "unit": "stream-frames/s",
                    "ms_per_frame_step": ms_b, "steps": reps * FB,
-                   "hbm_bytes_per_stream_frame": 8 * n_loc * k / FB + 12 * n_loc + 3 * P_loc,
-                   "note": "BatchTracker.push_many: U crosses HBM once per block of F frames "
-                           "(per-frame results identical to push; tests/test_gpu_parity.py)"}
+                   "hbm_bytes_per_stream_frame": (8 * n_loc * k / FB + 12 * n_loc + 3 * P_loc) if tmem_blk
+                   else (4 * 4 * n_loc * k + 24 * n_loc + 3 * P_loc),
+                   "phases_us_per_frame": {nm: 1000.0 * v[0] / FB for nm, v in ph_b.items() if v[1]},
+                   "note": ("BatchTracker.push_many: U crosses HBM once per block of F frames"
+                            if tmem_blk else
+                            "BatchTracker.push_many on the TMA-fed streamed kernels: each geodesic "
+                            "sweep also runs the next frame's pass 0 (4 passes over U per frame "
+                            "instead of 5)") +
+                           " (per-frame results identical to push; tests/test_gpu_parity.py)"}
 
     # per-phase breakdown (separate, untimed pass with events around launches)
     native.profile(True)

@@ -70,6 +70,7 @@ struct prost_handle {
   // streamed fp32 one-channel k > 20 (BASELINE C4): pass 0 / iteration /
   // gradient passes fed by tensor copies of U (prost_stream_tma.cuh)
   bool tma = false;
+  bool tma_next = false;  // k_geo_tma<K, true> (next frame's pass 0 fused) fits shared memory
   int tma_chunks = 0;
   CUtensorMap umap{};
   // device state
@@ -341,7 +342,10 @@ struct Impl {
           for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
           LAUNCH(PROST_PH_GRADFB, (k_gradfb_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
         }
-        LAUNCH(PROST_PH_GEO, (k_geo_tma<K><<<tg, TT, sg, st>>>(at, h->umap)));
+        if (a.xnext && h->tma_next && ((uintptr_t)a.xnext & 15) == 0)
+          LAUNCH(PROST_PH_GEO, (k_geo_tma<K, true><<<tg, TT, tma_smem_geo_next<K>(), st>>>(at, h->umap)));
+        else
+          LAUNCH(PROST_PH_GEO, (k_geo_tma<K><<<tg, TT, sg, st>>>(at, h->umap)));
       }
     }
     if (!fed) {
@@ -435,6 +439,12 @@ bool tma_attrs() {
          cudaFuncSetAttribute(k_geo_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg) == cudaSuccess;
 }
 
+template <int K>
+bool tma_attr_next() {
+  return cudaFuncSetAttribute(k_geo_tma<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)tma_smem_geo_next<K>()) == cudaSuccess;
+}
+
 void setup_tma(prost_handle* h, int sms) {
   const char* env = getenv("PROST_TMA");
   if ((env && env[0] == '0') || h->Pp % 16 != 0) return;
@@ -459,6 +469,10 @@ void setup_tma(prost_handle* h, int sms) {
     cudaGetLastError();
     return;
   }
+  // the geodesic sweep with the next frame's pass 0 (frame-blocked pushes):
+  // one more staged input per tile; used only if its shared memory fits
+  h->tma_next = h->ops.K == 30 ? tma_attr_next<30>() : h->ops.K == 32 ? tma_attr_next<32>() : false;
+  cudaGetLastError();
   // one CTA per SM (the tile ring takes most of shared memory), at most the
   // part slots the plain kernels use, at least one tile per CTA
   const long long tiles = (h->Pp + TT - 1) / TT;
@@ -667,7 +681,7 @@ int push_setup(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
   // 8-bit frames go to the TMEM kernel as they are (1 byte per coordinate in
   // HBM and over PCIe) and are divided by 255 on load; the other kernels read
   // a converted copy (k_pack)
-  const bool x8 = dtype == PROST_U8 && h->tmem && dense;
+  const bool x8 = dtype == PROST_U8 && (h->tmem || h->tma) && dense;
   if (x8) {
     if (on_device) xdev = frames;
     else CK(cudaMemcpyAsync(h->x, frames, (size_t)h->S * h->C * h->P, cudaMemcpyHostToDevice, st));
@@ -1211,6 +1225,7 @@ int prost_set_core_state(prost_handle* h, int32_t stream, const double* U, const
   if (y)
     for (int j = 0; j < k; ++j) c.y[j] = y[j];
   c.frame_index = frame_index;
+  c.p0_next = 0;
   c.since_qr = steps_since_qr;
   h->qr_bound = std::max<long long>(h->qr_bound, steps_since_qr);
   c.status = ST_OK;
@@ -1336,6 +1351,104 @@ int prost_push(prost_handle* h, const void* frames, int32_t dtype, int32_t on_de
 // prost_tmem.cuh): frames [F][S][C*P], outputs [F][S][...], fit [F][S].
 // Where the TMEM kernel cannot block (fp64, 3 channels, padded planes, the
 // periodic QR possibly inside the block) it runs F single-frame pushes.
+// prost_push_many on a TMA-fed streamed handle: the frames of the block run
+// in order with the device frames [F][S][n] and outputs [F][S][...] in place;
+// frame f's geodesic sweep also runs frame f+1's pass 0 (k_geo_tma<K, true>).
+int push_many_streamed(prost_handle* h, const void* frames, int nframes, int dtype, int on_device,
+                       const prost_outputs& o, cudaStream_t st) {
+  const int S = h->S;
+  const size_t n = (size_t)h->C * h->P;
+  const size_t fsz = dtype_size(dtype);
+  CK(cudaSetDevice(h->device));
+  {
+    int drc = io_drain(h);
+    if (drc) return drc;
+  }
+  retire_peek(h);
+  h->qr_due = false;
+  h->qr_bound += nframes;
+  const char* xdev = static_cast<const char*>(frames);
+  if (!on_device) {
+    const size_t bytes = (size_t)nframes * S * n * fsz;
+    int rc = grow(h, &h->xblk, &h->xblk_bytes, bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->xblk, frames, bytes, cudaMemcpyHostToDevice, st));
+    xdev = static_cast<const char*>(h->xblk);
+  }
+  const size_t obytes = (size_t)nframes * S * n * 4;
+  void* ouser[3] = {o.background, o.residual, o.fit_residual};
+  void* odev[3] = {nullptr, nullptr, nullptr};
+  for (int i = 0; i < 3; ++i) {
+    if (!ouser[i]) continue;
+    if (o.on_device) {
+      odev[i] = ouser[i];
+    } else {
+      if (h->oblk_bytes < obytes) {
+        for (int j = 0; j < 3; ++j) {
+          if (h->oblk[j]) cudaFree(h->oblk[j]);
+          h->oblk[j] = nullptr;
+        }
+        h->oblk_bytes = obytes;
+      }
+      if (!h->oblk[i]) CK(cudaMalloc(&h->oblk[i], h->oblk_bytes));
+      odev[i] = h->oblk[i];
+    }
+  }
+  const size_t lbytes = (size_t)nframes * S * h->Pp;
+  if (o.mask || o.raw_mask) {
+    if (h->lblk_bytes < lbytes) {
+      if (h->rawblk) cudaFree(h->rawblk);
+      if (h->maskblk) cudaFree(h->maskblk);
+      h->rawblk = h->maskblk = nullptr;
+      h->lblk_bytes = lbytes;
+    }
+    if (!h->rawblk) CK(cudaMalloc(&h->rawblk, h->lblk_bytes));
+    if (!h->maskblk) CK(cudaMalloc(&h->maskblk, h->lblk_bytes));
+  }
+  uint8_t* raw_d = (o.raw_mask && o.on_device) ? o.raw_mask : h->rawblk;
+  uint8_t* mask_d = (o.mask && o.on_device) ? o.mask : h->maskblk;
+  if (h->infoblk_n < (nframes + 1) * S) {
+    if (h->infoblk) cudaFree(h->infoblk);
+    h->infoblk = nullptr;
+    CK(cudaMalloc(&h->infoblk, (size_t)(nframes + 1) * S * sizeof(FitInfo)));
+    h->infoblk_n = (nframes + 1) * S;
+  }
+  const Args a0 = make_args(h, 0);
+  for (int f = 0; f < nframes; ++f) {
+    Args a = a0;
+    a.x = xdev + (size_t)f * S * n * fsz;
+    a.xu8 = dtype == PROST_U8 ? 1 : 0;
+    a.xnext = f + 1 < nframes ? xdev + (size_t)(f + 1) * S * n * fsz : nullptr;
+    a.info = h->infoblk + (size_t)f * S;
+    a.info_next = h->infoblk + (size_t)(f + 1) * S;
+    void** oarg[3] = {&a.bg_out, &a.res_out, &a.fitres_out};
+    for (int i = 0; i < 3; ++i)
+      if (odev[i]) *oarg[i] = static_cast<char*>(odev[i]) + (size_t)f * S * n * 4;
+    if (o.mask || o.raw_mask) a.raw_out = raw_d + (size_t)f * S * h->Pp;
+    if (o.mask) a.mask_out = mask_d + (size_t)f * S * h->Pp;
+    int rc = launch_frame(h, a, st);
+    if (rc) return rc;
+  }
+  if (!o.on_device) {
+    for (int i = 0; i < 3; ++i)
+      if (ouser[i]) CK(cudaMemcpyAsync(ouser[i], odev[i], obytes, cudaMemcpyDeviceToHost, st));
+    if (o.mask) CK(cudaMemcpyAsync(o.mask, h->maskblk, lbytes, cudaMemcpyDeviceToHost, st));
+    if (o.raw_mask) CK(cudaMemcpyAsync(o.raw_mask, h->rawblk, lbytes, cudaMemcpyDeviceToHost, st));
+  }
+  if (o.fit) {
+    CK(cudaMemcpyAsync(o.fit, h->infoblk, (size_t)nframes * S * sizeof(FitInfo), cudaMemcpyDeviceToHost, st));
+    if (!o.fit_async) {
+      CK(cudaStreamSynchronize(st));
+      bool cold = false;
+      for (int i = 0; i < nframes * S; ++i)
+        if (o.fit[i].status != PROST_OK) return fail(h, o.fit[i].status, "frame contains non-finite values");
+      for (int i = 0; i < S; ++i) cold |= o.fit[(size_t)(nframes - 1) * S + i].frame_index == 0;
+      h->maybe_cold = cold;
+    }
+  }
+  return PROST_OK;
+}
+
 int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_t dtype,
                     int32_t on_device, const prost_outputs* out, void* cuda_stream) {
   if (!h) return PROST_ERR_CONFIG;
@@ -1354,6 +1467,11 @@ int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_
   const bool dense = h->P == h->Pp;
   const bool blockable = nframes > 1 && h->tmem && h->C == 1 && dense && dtype != PROST_F64 &&
                          odt == PROST_F32 && h->qr_bound + nframes < QR_EVERY - 1;
+  // TMA-fed streamed handles (k > 20): the frames run one after another, each
+  // geodesic sweep carrying the next frame's pass 0 (one U pass fewer per frame)
+  const bool sblockable = nframes > 1 && !h->tmem && h->tma && h->tma_next && h->C == 1 && dense &&
+                          dtype != PROST_F64 && odt == PROST_F32 && h->qr_bound + nframes < QR_EVERY - 1;
+  if (sblockable) return push_many_streamed(h, frames, nframes, dtype, on_device, o, st);
   if (!blockable) {
     for (int f = 0; f < nframes; ++f) {
       prost_outputs of = o;

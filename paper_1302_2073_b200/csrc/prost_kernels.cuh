@@ -75,6 +75,11 @@ struct Ctl {
   int do_geo, qr_now, status, iterations, cost_evals, grad_evals, frozen, cold;
   int update_stats, no_info;  // no_info: this copy must not write FitInfo
   int info_slot;              // FitInfo row of this frame (frame-blocked pushes: f * S)
+  int pad0;
+  // frame-blocked streamed pushes: frame_index + 1 of the frame whose pass 0
+  // already ran inside the previous frame's geodesic sweep (k_geo_tma<K,
+  // true>); its statistics and pass-0 kernels then exit at once.  0: none.
+  long long p0_next;
 };
 
 struct FitInfo {  // layout-identical to prost_fit_info
@@ -89,6 +94,7 @@ struct Args {
   void* r;             // [S][np] residual (lazily updated)
   void* ud;            // [S][np] u_dir = U d of the last iteration
   const void* x;       // [S][np] frame (raw intensities or normalized x)
+  const void* xnext;   // frame-blocked streamed pushes: the next frame (same layout), or null
   void* mean;          // [S][np] running mean (pipeline)
   uint8_t* lab;        // [S][Pp] labels: 1 = foreground (weight omega)
   Ctl* ctl;            // [S]
@@ -96,6 +102,7 @@ struct Args {
   unsigned* cnt;       // [S]
   double* rinv;        // [S][KMAX][KMAX] inverse Cholesky factor (periodic QR)
   FitInfo* info;       // [S]
+  FitInfo* info_next;  // frame-blocked streamed pushes: the next frame's FitInfo rows
   void* bg_out;        // [S][np] or null
   void* res_out;       // [S][np] or null
   void* fitres_out;    // [S][np] fit residual x - U y before the geodesic (FitResult.residual) or null
@@ -578,6 +585,7 @@ __device__ PROST_LOGIC void fail_iteration(Ctl* c, const Args& a, int s, int lan
 
 __device__ __forceinline__ void mark_nonfinite(Ctl* c, const Args& a, int s, int lane) {
   if (lane == 0) {
+    c->p0_next = 0;
     c->status = ST_NONFINITE;
     c->active = 0;
     c->t = step_size(a, c->frame_index);

@@ -145,6 +145,10 @@ template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
+  if (c->p0_next == c->frame_index + 1) {  // this frame started in the previous geodesic sweep
+    mark_go(a, s, 0);
+    return;
+  }
   const bool upd = a.pipeline && !c->frozen && c->frame_index < a.i_init;
   mark_go(a, s, upd);
   if (!upd) {
@@ -168,11 +172,17 @@ __global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
   double s1 = 0.0, s2 = 0.0, nf = 0.0;
   const int ng = a.Pp / VEC;
   const T* X = static_cast<const T*>(a.x) + (size_t)s * a.np;
+  const uint8_t* X8 = static_cast<const uint8_t*>(a.x) + (size_t)s * a.np;
   for (int q = blockIdx.x * NT + threadIdx.x; q < ng; q += a.chunks * NT) {
     const int pix = q * VEC;
     for (int ch = 0; ch < a.C; ++ch) {
       T xv[VEC];
-      VecIO<T, VEC>::ldg(X + (size_t)ch * a.Pp + pix, xv);
+      if (a.xu8) {  // 8-bit frames read directly (TMA-fed streamed path), frameio.py:136
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) xv[e] = (T)((double)X8[(size_t)ch * a.Pp + pix + e] * (1.0 / 255.0));
+      } else {
+        VecIO<T, VEC>::ldg(X + (size_t)ch * a.Pp + pix, xv);
+      }
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         if (pix + e < a.P) {
@@ -254,7 +264,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_pass0(const __grid_constant_
   __shared__ int go, upd;
   __shared__ double sstd, sseen, sy[K];
   if (threadIdx.x == 0) {
-    go = c->status == ST_OK;
+    go = c->status == ST_OK && c->p0_next != c->frame_index + 1;
     upd = c->update_stats;
     sstd = c->std_cur;
     sseen = (double)c->pseen;

@@ -53,6 +53,8 @@ template <int K>
 __host__ __device__ constexpr size_t tma_smem_small() { return TStage<K, 2>::SMEM; }
 template <int K>
 __host__ __device__ constexpr size_t tma_smem_geo() { return TStage<K, 4>::SMEM; }
+template <int K>
+__host__ __device__ constexpr size_t tma_smem_geo_next() { return TStage<K, 5>::SMEM; }
 
 // The tile ring of one CTA over tiles blockIdx.x, blockIdx.x + chunks, ...
 // of stream s (rows s*k .. s*k+k-1 of the tensor map).
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(TT, 1) k_pass0_tma(const __grid_constant__ Arg
   __shared__ double sstd, sseen;
   __shared__ float sy[K];
   if (threadIdx.x == 0) {
-    go = c->status == ST_OK;
+    go = c->status == ST_OK && c->p0_next != c->frame_index + 1;
     upd = c->update_stats;
     sstd = c->std_cur;
     sseen = (double)c->pseen;
@@ -432,14 +434,26 @@ __global__ void __launch_bounds__(TT, 1) k_gradfb_tma(const __grid_constant__ Ar
 // rank-one geodesic step of U (manifold.py:130-197) and the relabel /
 // background / residual epilogue (pipeline.py:158-175) — k_geo<float, K, 1,
 // false> with the basis tile updated in shared memory and stored back by TMA.
-template <int K>
+//
+// NEXT (frame-blocked pushes, a.xnext = the next frame): pass 0 of the next
+// frame runs in the same sweep, on U' while it is in shared memory, with the
+// labels just computed as its weights and this frame's y as its warm start —
+// r0 = x_{f+1}/std - U'y is the relabel's U'y (same operation order as
+// k_pass0_tma, so the same bits), saving one pass over U per frame.  Only when
+// the next frame does not update the running statistics (its normalization is
+// then known here) and no periodic QR follows this frame; the last CTA does
+// the next frame's start (what k_stats does for a frozen stream) and
+// after_pass0, and marks the frame (Ctl::p0_next) so its own statistics and
+// pass-0 kernels exit at once.  A non-finite next frame is left to its own
+// pass 0 (which reports it).
+template <int K, bool NEXT = false>
 __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args a,
                                                    const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(128) uint8_t tsm[];
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
-  __shared__ int go, dogeo, relabel;
-  __shared__ double sc[5];
+  __shared__ int go, dogeo, relabel, fuse;
+  __shared__ double sc[6];
   __shared__ __align__(16) float sv[K], sg[K], sy[K];
   if (threadIdx.x == 0) {
     go = c->status == ST_OK;
@@ -450,6 +464,14 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
     sc[2] = c->geo_ln;
     sc[3] = c->pend_alpha;
     sc[4] = c->std_cur;
+    int fu = 0;
+    if (NEXT && a.xnext && go && relabel) {
+      // the next frame (frame_index was advanced by this frame's finish)
+      const bool upd1 = a.pipeline && !c->frozen && c->frame_index < a.i_init;
+      fu = !upd1;
+      sc[5] = !a.pipeline ? 1.0 : (c->frozen ? c->pstd : running_std(c));
+    }
+    fuse = fu;
   }
   if (threadIdx.x < K) {
     const int j = threadIdx.x;
@@ -462,14 +484,16 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
   const float ga = (float)sc[0], gsn = (float)sc[1], ln = (float)sc[2], pend = (float)sc[3],
               stdv = (float)sc[4];
   const bool moved = sc[3] != 0.0;
-  const bool do_geo = dogeo, do_lab = relabel;
+  const bool do_geo = dogeo, do_lab = relabel, fu = NEXT && fuse;
   float* FRES = a.fitres_out ? static_cast<float*>(a.fitres_out) + (size_t)s * a.np : nullptr;
   float* RES = a.res_out ? static_cast<float*>(a.res_out) + (size_t)s * a.np : nullptr;
   float* BG = a.bg_out ? static_cast<float*>(a.bg_out) + (size_t)s * a.np : nullptr;
+  float* RR = static_cast<float*>(a.r) + (size_t)s * a.np;
   uint8_t* L = a.lab + (size_t)s * a.Pp;
   uint8_t* RAW = a.raw_out ? a.raw_out + (size_t)s * a.Pp : nullptr;
   const bool need_r = FRES || do_geo;
-  Ring<K, 4> R;
+  constexpr int NS = NEXT ? 5 : 4;
+  Ring<K, NS> R;
   ring_geometry(R, a, s, &map);
   if (need_r) R.side[0] = static_cast<const uint8_t*>(a.r) + (size_t)s * a.np * 4;
   if (need_r && moved) R.side[1] = static_cast<const uint8_t*>(a.ud) + (size_t)s * a.np * 4;
@@ -478,7 +502,22 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
     R.side_es[2] = a.xu8 ? 1 : 4;
     if (a.pipeline) R.side[3] = static_cast<const uint8_t*>(a.mean) + (size_t)s * a.np * 4;
   }
+  if constexpr (NEXT) {
+    if (fu) {
+      R.side[4] = static_cast<const uint8_t*>(a.xnext) + (size_t)s * a.np * (a.xu8 ? 1 : 4);
+      R.side_es[4] = a.xu8 ? 1 : 4;
+    }
+  }
   R.start(tsm);
+  // next frame's pass 0 (NEXT): cost, coordinate gradient, ||g||^2, non-finite
+  constexpr int KN = NEXT ? K : 1;
+  float acc1[KN];
+#pragma unroll
+  for (int j = 0; j < KN; ++j) acc1[j] = 0.f;
+  double cost1 = 0.0;
+  float gsq1 = 0.f;
+  bool bad1 = false;
+  const float std1 = NEXT ? (float)sc[5] : 1.f;
   const int t = threadIdx.x;
   for (int i = 0; i < R.ntiles; ++i) {
     R.wait(i);
@@ -514,8 +553,7 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
         const float xh = tile_xhat(a, R.sideb(st, 2), R.sidef(st, 3), t, nullptr, pix, false, 1.f, stdv, bad);
         float acc = 0.f;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-          acc += *R.urow(st, j, t) * sy[j];
+        for (int j = 0; j < K; ++j) acc += *R.urow(st, j, t) * sy[j];
         const float rr = sub_rn(xh, acc);
         const float mx = fmaxf(0.f, fabsf(rr));
         if (RES) RES[pix] = rr;
@@ -523,6 +561,20 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
         const uint8_t lb = (pix < a.P && (double)mx >= a.delta) ? 1 : 0;
         L[pix] = lb;
         if (RAW) RAW[pix] = lb;
+        if constexpr (NEXT) {
+          if (fu) {  // pass 0 of the next frame (k_pass0_tma's operations)
+            const float w1 = tile_weight(a, pix, lb);
+            const float xh1 = tile_xhat(a, R.sideb(st, 4), R.sidef(st, 3), t, nullptr, pix, false, 1.f, std1, bad1);
+            const float r0 = sub_rn(xh1, acc);
+            float tw, g;
+            penalty(r0, w1, a, tw, g);
+            cost1 += (double)tw;
+            gsq1 += g * g;
+#pragma unroll
+            for (int j = 0; j < K; ++j) acc1[j] += *R.urow(st, j, t) * g;
+            RR[pix] = r0;
+          }
+        }
       }
     }
     if (do_geo) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // U' visible to the store
@@ -546,6 +598,34 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
     }
   }
   if (threadIdx.x == 0 && do_geo) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if constexpr (NEXT) {
+    if (!fu) return;
+    constexpr int NV = K + 3;
+    __shared__ double sm[(TT / 32) * NV];
+    __shared__ double red[NV];
+    cta_stage<TT>(cost1, sm, 0, NV);
+#pragma unroll
+    for (int j = 0; j < K; ++j) cta_stage<TT>((double)acc1[j], sm, 1 + j, NV);
+    cta_stage<TT>((double)gsq1, sm, K + 1, NV);
+    cta_stage<TT>(bad1 ? 1.0 : 0.0, sm, K + 2, NV);
+    if (!cta_finish<TT>(a, s, sm, NV, red)) return;
+    if (threadIdx.x < 32 && red[K + 2] == 0.0) {
+      if (threadIdx.x == 0) {  // the next frame's start (k_stats, frozen stream)
+        if (a.pipeline && !c->frozen) {
+          c->frozen = 1;
+          c->pstd = sc[5];
+        }
+        c->std_cur = sc[5];
+        c->update_stats = 0;
+        c->status = ST_OK;
+        c->p0_next = c->frame_index + 1;
+      }
+      __syncwarp();
+      Args an = a;  // the next frame's FitInfo rows (a fit that ends at pass 0 reports there)
+      an.info = a.info_next;
+      after_pass0<K>(c, an, s, threadIdx.x, red);
+    }
+  }
 }
 
 }  // namespace prost

@@ -606,16 +606,22 @@ def test_off_resolution_frames_stay_on_device():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["f32", "u8"])
-def test_frame_blocking_matches_single_frame_pushes(dtype):
-    """push_many (F frames per stream, the slice kept on chip across them, the
-    next frame's pass 0 run inside the geodesic sweep) gives bit-identical
-    masks, raw masks, backgrounds, residuals, FitInfo and bases to pushing
-    the same frames one at a time — across the statistics window (separate
-    pass 0 there) and past it (fused)."""
+@pytest.mark.parametrize("path", ["tmem", "tma"])
+def test_frame_blocking_matches_single_frame_pushes(dtype, path):
+    """push_many (F frames per stream; the next frame's pass 0 run inside the
+    geodesic sweep) gives bit-identical masks, raw masks, backgrounds,
+    residuals, FitInfo and bases to pushing the same frames one at a time —
+    across the statistics window (separate pass 0 there) and past it (fused).
+    path "tmem": the slice kept on chip across the frames (k = 15); "tma": the
+    TMA-fed streamed kernels (k = 30), k_geo_tma<K, true>."""
     import torch
+    from paper_1302_2073_b200 import _native as nat
 
-    W, H, S, F, B = 64, 48, 6, 12, 4
-    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+    if path == "tmem":
+        W, H, S, F, B, K = 64, 48, 6, 12, 4, 15
+    else:
+        W, H, S, F, B, K = 128, 64, 2, 12, 4, 30
+    cfg = pkg.RunConfig(subspace_dim=K, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
                         target_height=H, grayscale=True, i_init=5, seed=0)
     data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1)  # [F, S, n]
     if dtype == "u8":
@@ -624,6 +630,8 @@ def test_frame_blocking_matches_single_frame_pushes(dtype):
         data = data.astype(np.float32)
     one = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
     blk = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+    if path == "tma":
+        assert blk.native.query(nat.Q_TMA) > 0
     n = W * H
     ref = {k: [] for k in ("mask", "raw", "bg", "res", "cost", "fi")}
     m1 = torch.empty((S, n), dtype=torch.uint8, device="cuda")
