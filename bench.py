@@ -376,7 +376,7 @@ def main():
 
     preroll = cfg.i_init if args.preroll is None else args.preroll
     e2e_frames = 0 if args.no_e2e else 2 + args.steps
-    nblock = 0 if args.block <= 1 else args.block * (max(1, args.steps // args.block) + 1)
+    nblock = 0 if args.block <= 1 else args.block * (max(1, args.steps // args.block) + 2)
     need = preroll + args.warmup + args.steps + 3 + e2e_frames + nblock
     t_gen = time.perf_counter()
     if args.frames > 0:
