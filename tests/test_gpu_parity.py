@@ -664,3 +664,12 @@ def test_frame_blocking_matches_single_frame_pushes(dtype, path):
             assert [info[i * S + s].frame_index for s in range(S)] == ref["fi"][f]
     for s in range(S):
         np.testing.assert_array_equal(blk.native.get_core_state(s)[0], one.native.get_core_state(s)[0])
+    if path == "tma":  # host frames and host outputs through the same blocked path
+        hst = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        mh = np.empty((B, S, n), dtype=np.uint8)
+        bh = np.empty((B, S, n), dtype=np.float32)
+        for f0 in range(0, F, B):
+            hst.push_many(np.ascontiguousarray(data[f0:f0 + B]), background=bh, mask=mh)
+            for i in range(B):
+                np.testing.assert_array_equal(mh[i], ref["mask"][f0 + i])
+                np.testing.assert_array_equal(bh[i], ref["bg"][f0 + i])
