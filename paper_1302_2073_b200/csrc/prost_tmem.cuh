@@ -58,6 +58,9 @@
 #ifndef PROST_TM_CPS
 #define PROST_TM_CPS 1
 #endif
+#ifndef PROST_SKEW_PROBE
+#define PROST_SKEW_PROBE 0
+#endif
 #ifndef PROST_RCP_STD
 #define PROST_RCP_STD 1  // normalize with the reciprocal of the std (<= 1 ulp from x / std)
 #endif
@@ -192,11 +195,25 @@ __device__ __forceinline__ void team_sum_g(const RArgs& ra, int vt, int VT, int 
   if (lt == 0) {
     unsigned* ctr = ra.bar + vt;
     const unsigned target = epoch * (unsigned)G;
+#if PROST_SKEW_PROBE
+    // experiment build: the last CTA to arrive times the bare round trip
+    // (PROF_SW_OWN / PROF_SW_ALL are repurposed)
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    const bool last_in = old + 1 == target;
+#else
     red_release_add(ctr, 1u);
+#endif
     long long spins = 0;
     while (ld_acquire(ctr) < target) {
       if (++spins > (1LL << 26)) __trap();
     }
+#if PROST_SKEW_PROBE
+    if (tp && last_in) {
+      sprof[PROF_SW_OWN] += ptimer() - t0;
+      sprof[PROF_SW_ALL] += 1000;
+    }
+#endif
   }
   group_sync<NG>(g);
   unsigned long long t1 = tp ? ptimer() : 0;
@@ -942,8 +959,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           const unsigned long long t1 = tid == 0 ? ptimer() : 0;
           group_sync<NG>(g);
           if (tid == 0) {
+#if !PROST_SKEW_PROBE
             sprof[PROF_SW_OWN] += t1 - tsw0;
             sprof[PROF_SW_ALL] += ptimer() - tsw0;
+#endif
           }
         }
         team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
