@@ -488,13 +488,17 @@ def test_pipelined_host_io_matches_device_io():
 
 
 @pytest.mark.gpu
-def test_u8_frame_ingest():
+@pytest.mark.parametrize("k", [8, 30])
+def test_u8_frame_ingest(k):
     """8-bit frames are divided by 255 on load (frameio.py:136, SURVEY §8(f)
-    row 1): the same result as pushing the scaled float32 frames."""
+    row 1): the same result as pushing the scaled float32 frames — the TMEM
+    kernel (k = 8) and the TMA-fed streamed kernels (k = 30: statistics,
+    pass 0, geodesic sweep read the bytes themselves)."""
     import torch
+    from paper_1302_2073_b200 import _native as nat
 
-    W, H, S, F = 64, 48, 3, 6
-    cfg = pkg.RunConfig(subspace_dim=8, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+    W, H, S, F = (64, 48, 3, 6) if k == 8 else (128, 64, 2, 8)
+    cfg = pkg.RunConfig(subspace_dim=k, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
                         target_height=H, grayscale=True, i_init=3, seed=0)
     data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1)
     q = np.clip(np.rint(data * 255.0), 0, 255).astype(np.uint8)
@@ -502,6 +506,7 @@ def test_u8_frame_ingest():
     outs = []
     for frames in (q, scaled):
         bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        assert (bt.native.query(nat.Q_TMA) > 0) == (k == 30)
         mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
         bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
         for f in range(F):
