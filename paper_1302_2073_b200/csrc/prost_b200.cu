@@ -17,6 +17,7 @@
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/prost_b200.h"
@@ -62,6 +63,7 @@ struct prost_handle {
   int rG = 0, rT = 0, rqpc = 0, rnt = 0;
   int rng = 1;  // k_tmem slot groups per CTA
   bool tm_cl = false;  // k_tmem teams as thread-block clusters (team sums over DSMEM)
+  bool pdl = false;    // streamed phase kernels with programmatic dependent launch (PROST_PDL)
   size_t rsmem = 0;
   unsigned* rbar = nullptr;
   double* rpart = nullptr;
@@ -294,19 +296,41 @@ struct PhaseTimer {
 };
 
 // 3x3 majority filter of the raw labels into a.mask_out (pipeline.py:215-228)
-void launch_median(prost_handle* h, const Args& a, cudaStream_t st, int sw) {
+// Launch a phase kernel; pdl: with programmatic stream serialization (the
+// kernel starts with pdl_enter, prost_kernels.cuh), so its launch and ramp
+// overlap the predecessor's drain.
+template <typename... P, typename... A>
+void launchk(bool pdl, void (*k)(P...), dim3 g, dim3 b, size_t sm, cudaStream_t st, A&&... args) {
+  if (!pdl) {
+    k<<<g, b, sm, st>>>(std::forward<A>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
+void launch_median(prost_handle* h, const Args& a, cudaStream_t st, int sw, bool pdl = false) {
   const uintptr_t al = (uintptr_t)a.mask_out | (uintptr_t)a.halo_top | (uintptr_t)a.halo_bot;
   if (h->prm.width % 16 == 0 && (al & 15) == 0 && h->Pp % 16 == 0) {
     const int nw = h->P / 16;
     const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
-    k_median16<<<mg, NT, 0, st>>>(a);
+    launchk(pdl, k_median16, mg, dim3(NT), 0, st, a);
   } else if (h->prm.width % 4 == 0 && ((uintptr_t)a.mask_out & 3) == 0) {
     const int nw = h->P / 4;
     const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
-    k_median4<<<mg, NT, 0, st>>>(a);
+    launchk(pdl, k_median4, mg, dim3(NT), 0, st, a);
   } else {
     const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), sw);
-    k_median<<<mg, NT, 0, st>>>(a);
+    launchk(pdl, k_median, mg, dim3(NT), 0, st, a);
   }
 }
 
@@ -324,8 +348,8 @@ struct Impl {
   static void frame(prost_handle* h, Args& a, cudaStream_t st, int sw) {
     const dim3 grid(h->chunks, sw);
     long long n = 0;
-    LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a)));
-    if (h->maybe_cold) LAUNCH(PROST_PH_COLD, (k_cold<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+    LAUNCH(PROST_PH_STATS, (launchk(h->pdl, k_stats<T, VEC>, grid, dim3(NT), 0, st, a)));
+    if (h->maybe_cold) LAUNCH(PROST_PH_COLD, (launchk(h->pdl, k_cold<T, K, VEC>, grid, dim3(NT), 0, st, a)));
     // tensor-copy-fed U passes (prost_stream_tma.cuh): frame pointer aligned
     // for the 1-D bulk copies
     bool fed = false;
@@ -336,34 +360,34 @@ struct Impl {
         at.chunks = h->tma_chunks;
         const dim3 tg(h->tma_chunks, sw);
         constexpr size_t sm = tma_smem_small<K>(), sg = tma_smem_geo<K>();
-        LAUNCH(PROST_PH_PASS0, (k_pass0_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
+        LAUNCH(PROST_PH_PASS0, (launchk(h->pdl, k_pass0_tma<K>, tg, dim3(TT), sm, st, at, h->umap)));
         for (int it = 0; it < h->prm.cg_max_iters; ++it) {
-          LAUNCH(PROST_PH_ITER, (k_iter_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
-          for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
-          LAUNCH(PROST_PH_GRADFB, (k_gradfb_tma<K><<<tg, TT, sm, st>>>(at, h->umap)));
+          LAUNCH(PROST_PH_ITER, (launchk(h->pdl, k_iter_tma<K>, tg, dim3(TT), sm, st, at, h->umap)));
+          for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (launchk(h->pdl, k_lsfb<T, VEC>, grid, dim3(NT), 0, st, a)));
+          LAUNCH(PROST_PH_GRADFB, (launchk(h->pdl, k_gradfb_tma<K>, tg, dim3(TT), sm, st, at, h->umap)));
         }
         if (a.xnext && h->tma_next && ((uintptr_t)a.xnext & 15) == 0)
-          LAUNCH(PROST_PH_GEO, (k_geo_tma<K, true><<<tg, TT, tma_smem_geo_next<K>(), st>>>(at, h->umap)));
+          LAUNCH(PROST_PH_GEO, (launchk(h->pdl, k_geo_tma<K, true>, tg, dim3(TT), tma_smem_geo_next<K>(), st, at, h->umap)));
         else
-          LAUNCH(PROST_PH_GEO, (k_geo_tma<K><<<tg, TT, sg, st>>>(at, h->umap)));
+          LAUNCH(PROST_PH_GEO, (launchk(h->pdl, k_geo_tma<K>, tg, dim3(TT), sg, st, at, h->umap)));
       }
     }
     if (!fed) {
-      LAUNCH(PROST_PH_PASS0, (k_pass0<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+      LAUNCH(PROST_PH_PASS0, (launchk(h->pdl, k_pass0<T, K, VEC>, grid, dim3(NT), 0, st, a)));
       for (int it = 0; it < h->prm.cg_max_iters; ++it) {
-        LAUNCH(PROST_PH_ITER, (k_iter<T, K, VEC><<<grid, NT, 0, st>>>(a)));
-        for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (k_lsfb<T, VEC><<<grid, NT, 0, st>>>(a)));
-        LAUNCH(PROST_PH_GRADFB, (k_gradfb<T, K, VEC><<<grid, NT, 0, st>>>(a)));
+        LAUNCH(PROST_PH_ITER, (launchk(h->pdl, k_iter<T, K, VEC>, grid, dim3(NT), 0, st, a)));
+        for (int l = 0; l < h->n_ls; ++l) LAUNCH(PROST_PH_LSFB, (launchk(h->pdl, k_lsfb<T, VEC>, grid, dim3(NT), 0, st, a)));
+        LAUNCH(PROST_PH_GRADFB, (launchk(h->pdl, k_gradfb<T, K, VEC>, grid, dim3(NT), 0, st, a)));
       }
-      LAUNCH(PROST_PH_GEO, (k_geo<T, K, VEC, false><<<grid, NT, 0, st>>>(a)));
+      LAUNCH(PROST_PH_GEO, (launchk(h->pdl, k_geo<T, K, VEC, false>, grid, dim3(NT), 0, st, a)));
     }
     if (h->qr_due) {
-      LAUNCH(PROST_PH_QR, (k_gram<T, K, VEC><<<grid, NT, 0, st>>>(a)));
-      LAUNCH(PROST_PH_QR, (k_geo<T, K, VEC, true><<<grid, NT, 0, st>>>(a)));
+      LAUNCH(PROST_PH_QR, (launchk(h->pdl, k_gram<T, K, VEC>, grid, dim3(NT), 0, st, a)));
+      LAUNCH(PROST_PH_QR, (launchk(h->pdl, k_geo<T, K, VEC, true>, grid, dim3(NT), 0, st, a)));
     }
     if (a.mask_out) {
-      if (a.xpeer && a.xhalo) LAUNCH(PROST_PH_MEDIAN, (k_halo_push<<<dim3(1, sw), NT, 0, st>>>(a)));
-      LAUNCH(PROST_PH_MEDIAN, launch_median(h, a, st, sw));
+      if (a.xpeer && a.xhalo) LAUNCH(PROST_PH_MEDIAN, (launchk(h->pdl, k_halo_push, dim3(1, sw), dim3(NT), 0, st, a)));
+      LAUNCH(PROST_PH_MEDIAN, launch_median(h, a, st, sw, h->pdl));
     }
     h->launches += n;
   }
@@ -943,6 +967,10 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   h->np = (long long)h->C * h->Pp;
   h->esz = h->fp64 ? 8 : 4;
   h->ops = h->fp64 ? pick<double>(h->k) : pick<float>(h->k);
+  {
+    const char* pe = getenv("PROST_PDL");
+    h->pdl = pe ? pe[0] == '1' : true;  // C4: 0.966 -> 0.942 ms per frame
+  }
   *out = h;
   if (!h->ops.frame) return fail(h, PROST_ERR_CONFIG, "no kernel instance for k=%d", h->k);
   const int K = h->ops.K;

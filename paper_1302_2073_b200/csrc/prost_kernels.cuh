@@ -373,6 +373,15 @@ __device__ __noinline__ void xpeer_exchange(const Args& a, int s, int nv, double
   __syncthreads();
 }
 
+// Programmatic dependent launch: a phase kernel launched with programmatic
+// stream serialization may be scheduled while its predecessor drains; it
+// waits here for the predecessor's completion and memory, then allows its own
+// successor to be scheduled.  Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // NTH: threads of the CTA (the TMA-fed streamed kernels run 512).
 template <int NTH = NT>
 __device__ __forceinline__ void cta_stage(double x, double* sm, int slot, int nv) {

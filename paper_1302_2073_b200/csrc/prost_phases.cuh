@@ -143,6 +143,7 @@ __device__ __forceinline__ void tail_gram(Ctl* c, const Args& a, int s, const do
 
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   if (c->p0_next == c->frame_index + 1) {  // this frame started in the previous geodesic sweep
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(NT) k_stats(const __grid_constant__ Args a) {
 
 template <typename T, int K, int VEC>
 __global__ void __launch_bounds__(NT) k_cold(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, upd;
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__(NT) k_cold(const __grid_constant__ Args a) {
 
 template <typename T, int K, int VEC>
 __global__ void __launch_bounds__(NT, PROST_MINB) k_pass0(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, upd;
@@ -340,6 +343,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_pass0(const __grid_constant_
 
 template <typename T, int K, int VEC>
 __global__ void __launch_bounds__(NT, PROST_MINB) k_iter(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, lo;
@@ -464,6 +468,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_iter(const __grid_constant__
 
 template <typename T, int VEC>
 __global__ void __launch_bounds__(NT) k_lsfb(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, m0;
@@ -527,6 +532,7 @@ __global__ void __launch_bounds__(NT) k_lsfb(const __grid_constant__ Args a) {
 
 template <typename T, int K, int VEC>
 __global__ void __launch_bounds__(NT, PROST_MINB) k_gradfb(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go;
@@ -592,6 +598,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_gradfb(const __grid_constant
 
 template <typename T, int K, int VEC, bool QR>
 __global__ void __launch_bounds__(NT, PROST_MINB) k_geo(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go, dogeo, relabel;
@@ -764,6 +771,7 @@ __global__ void __launch_bounds__(NT, PROST_MINB) k_geo(const __grid_constant__ 
 
 template <typename T, int K, int VEC>
 __global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
   __shared__ int go;
@@ -805,6 +813,7 @@ __global__ void __launch_bounds__(NT) k_gram(const __grid_constant__ Args a) {
 // rank's first label row goes to the rank above (its row below), its last row
 // to the rank below (its row above); the flag carries the frame number.
 static __global__ void __launch_bounds__(NT) k_halo_push(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   const int W = a.width, H = a.height, par = (int)(a.xframe & 1);
   const uint8_t* L = a.lab + (size_t)s * a.Pp;
@@ -838,6 +847,7 @@ __device__ __forceinline__ void halo_wait(const Args& a, int s) {
 // k_median: 3x3 majority vote with edge replication (pipeline.py:215-228).
 
 static __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   halo_wait(a, s);
@@ -869,6 +879,7 @@ static __global__ void __launch_bounds__(NT) k_median(const __grid_constant__ Ar
 // horizontal window adds the word shifted by one byte each way, with the
 // neighbouring columns (edge-replicated) shifted in; >= 5 is __vcmpgeu4.
 static __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   halo_wait(a, s);
@@ -899,6 +910,7 @@ static __global__ void __launch_bounds__(NT) k_median4(const __grid_constant__ A
 // k_median16: sixteen pixels per thread (widths that are a multiple of 16):
 // three 16-byte row loads and two edge bytes per row per 16 pixels.
 static __global__ void __launch_bounds__(NT) k_median16(const __grid_constant__ Args a) {
+  pdl_enter();
   const int s = a.s0 + blockIdx.y;
   if (a.ctl[s].status != ST_OK) return;
   halo_wait(a, s);

@@ -208,6 +208,7 @@ __device__ __forceinline__ float tile_xhat(const Args& a, const uint8_t* xs, con
 template <int K>
 __global__ void __launch_bounds__(TT, 1) k_pass0_tma(const __grid_constant__ Args a,
                                                      const __grid_constant__ CUtensorMap map) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t tsm[];
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
@@ -280,6 +281,7 @@ __global__ void __launch_bounds__(TT, 1) k_pass0_tma(const __grid_constant__ Arg
 template <int K>
 __global__ void __launch_bounds__(TT, 1) k_iter_tma(const __grid_constant__ Args a,
                                                     const __grid_constant__ CUtensorMap map) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t tsm[];
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
@@ -383,6 +385,7 @@ __global__ void __launch_bounds__(TT, 1) k_iter_tma(const __grid_constant__ Args
 template <int K>
 __global__ void __launch_bounds__(TT, 1) k_gradfb_tma(const __grid_constant__ Args a,
                                                       const __grid_constant__ CUtensorMap map) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t tsm[];
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
@@ -449,6 +452,7 @@ __global__ void __launch_bounds__(TT, 1) k_gradfb_tma(const __grid_constant__ Ar
 template <int K, bool NEXT = false>
 __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args a,
                                                    const __grid_constant__ CUtensorMap map) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t tsm[];
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
