@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     }
   };
 
+  if constexpr (CL) pdl_enter();  // cluster teams run with programmatic dependent launch
   if (tid < PROF_N) sprof[tid] = 0;
   if (tid < 2) {
     s_loads[tid] = 0;

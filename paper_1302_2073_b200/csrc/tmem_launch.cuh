@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernel_ops.h"
 #include "prost_tmem.cuh"
@@ -12,6 +13,14 @@
 namespace prost_ops {
 
 using namespace prost;
+
+inline bool tm_pdl() {
+  static const bool on = [] {
+    const char* e = getenv("PROST_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 template <int K, int PM, int NG, bool BLK, bool CL>
 struct Tm {
@@ -28,13 +37,17 @@ struct Tm {
       cfg.blockDim = dim3(TM_NT);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
-      cudaLaunchAttribute at[1];
+      // programmatic dependent launch: the next frame's clusters are placed
+      // on free SMs while this one drains and wait in pdl_enter
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = ra.G;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = (ra.prof || !tm_pdl()) ? 1 : 2;
       return cudaLaunchKernelExC(&cfg, (const void*)kernel, args);
     }
     if (TM_CPS == 1)
