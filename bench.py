@@ -441,12 +441,17 @@ def main():
                           if args.exchange == "peer" else
                           "kernels, NCCL all-reduce of the phase partials (host-driven program)"))
     elif mode:
+        cl = native.query(nat.Q_CLUSTER)
         kernel_path = (f"{'tmem' if mode == 2 else 'register'}-resident: "
                        f"{native.query(nat.Q_TEAMS)} teams x "
                        f"{native.query(nat.Q_TEAM)} CTAs x {native.query(nat.Q_GROUPS)} slot groups, "
-                       "one cooperative launch per step")
+                       + ("each team one thread-block cluster (DSMEM team sums), one launch per step"
+                          if cl else "one cooperative launch per step"))
     else:
-        kernel_path = f"streamed: {native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel"
+        tma = native.query(nat.Q_TMA)
+        kernel_path = (f"streamed, TMA-fed: {tma} CTAs x 512 threads per stream per U pass "
+                       "(tensor-map tiles + bulk copies)" if tma else
+                       f"streamed: {native.query(nat.Q_CHUNKS)} CTAs per stream per phase kernel")
     mask = torch.empty((S, P_loc), dtype=torch.uint8, device=f"cuda:{dev}")
     bg = torch.empty((S, n_loc), dtype=torch.float32 if args.precision == "fp32" else torch.float64,
                      device=f"cuda:{dev}")
