@@ -821,7 +821,8 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
              h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, pfe ? atoi(pfe) : 0,
              alt ? atoi(alt) : 1};
-    if (!h->tm_cl) CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
+    // team barrier counters, the stream counter and the teams' next streams
+    if (!h->tm_cl) CK(cudaMemsetAsync(h->rbar, 0, (size_t)(3 * h->rT * h->rng + 1) * sizeof(unsigned), st));
     // cluster teams filter the labels themselves (one channel, 4-pixel words)
     // (not when the periodic QR may run after the kernel: it relabels)
     const bool med_in =
@@ -1578,7 +1579,7 @@ int prost_push_many(prost_handle* h, const void* frames, int32_t nframes, int32_
   const char* stg = getenv("PROST_STAGGER_NS");
   RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
            h->prof ? h->rprof : nullptr, stg ? atoi(stg) : 0, 0, 1};
-  CK(cudaMemsetAsync(h->rbar, 0, (size_t)h->rT * h->rng * sizeof(unsigned), st));
+  CK(cudaMemsetAsync(h->rbar, 0, (size_t)(3 * h->rT * h->rng + 1) * sizeof(unsigned), st));
   {
     PhaseTimer pt_(h, st, PROST_PH_FRAME);
     CK(pick_tmem(h->resident_ops_K, h->prm.p == 0.5, h->rng, true).launch(a, ra, h->rsmem, st));

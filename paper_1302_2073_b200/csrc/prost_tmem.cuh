@@ -58,6 +58,9 @@
 #ifndef PROST_TM_CPS
 #define PROST_TM_CPS 1
 #endif
+#ifndef PROST_DYN
+#define PROST_DYN 1  // dynamic stream-to-team assignment (see the round loop)
+#endif
 #ifndef PROST_SKEW_PROBE
 #define PROST_SKEW_PROBE 0
 #endif
@@ -501,7 +504,25 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   }
 
   int round = 0;
+#if PROST_DYN
+  // Dynamic stream assignment: a team's first stream is vt, then rank 0
+  // takes the next one from a global counter (ra.bar[VT]) at the start of each
+  // round and publishes it (ra.bar[VT + 1 + 2 vt + parity]) before the round's first team
+  // sum, whose release/acquire barrier makes it visible to the team — teams
+  // that draw cheap streams take more (a stream's result does not depend on
+  // its team: every team has the same geometry).
+  for (int s = vt; s < ra.S; ++round) {
+    if (!CL && NG == 1 && rank == 0 && lt == 0) {
+      // slot by round parity: a team mate may still be reading this round's
+      // stream (published last round) while rank 0 publishes the next one
+      const unsigned nx = (unsigned)VT + atomicAdd(ra.bar + VT, 1u);
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ra.bar + VT + 1 + 2 * vt + ((round + 1) & 1)),
+                   "r"(nx)
+                   : "memory");
+    }
+#else
   for (int s = vt; s < ra.S; s += VT, ++round) {
+#endif
     if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
     if (NG > 1 && ra.alt) {
       // the groups' slice loads alternate: A0 B0 A1 B1 ... (a finished group
@@ -1158,6 +1179,18 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         }
       }
     }
+#if PROST_DYN
+    if constexpr (CL || NG > 1) {
+      s += VT;
+    } else {
+      unsigned nx;
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];"
+                   : "=r"(nx)
+                   : "l"(ra.bar + VT + 1 + 2 * vt + ((round + 1) & 1))
+                   : "memory");
+      s = (int)nx;
+    }
+#endif
   }
   if (NG > 1 && lt == 0) s_done[g] = 1;
 #undef LOGIC
