@@ -32,7 +32,7 @@ struct RArgs {
   int S;            // streams
   unsigned long long* prof;  // [gridDim][8] optional timing counters (ns), or null
   int stagger_ns;            // start delay of odd teams (k_tmem), 0 = none
-  int prefetch;              // k_tmem: L2 prefetch of the next stream's slice
+  int prefetch;              // k_tmem: L2 prefetch of the slots after the first of a CTA's slice
   int alt;                   // k_tmem with 2 slot groups: alternate the groups' slice loads
   int median;                // k_tmem cluster teams: the 3x3 label median in-kernel (mask_out)
 };

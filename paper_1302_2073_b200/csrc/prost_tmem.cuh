@@ -698,6 +698,26 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     if (frame_ok && f == 0) {
       const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
       const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
+      // The slots after the first arrive through L2: one bulk prefetch per
+      // basis plane (and for the frame / mean / label bytes) of the rest of
+      // this CTA's slice, issued before slot 0's loads, so HBM streams the
+      // whole slice while the threads work through the slots in order.
+      if (ra.prefetch && (lt >> 5) == 0 && nslots > 1) {
+        const int lane = lt & 31;
+        const long long c0 = (long long)(q0 + TG) * 4, c1 = (long long)(q0 + qcount) * 4;
+        auto pf = [&](const void* base, long long b0, long long b1) {
+          const uintptr_t p0 = ((uintptr_t)base + b0 + 15) & ~(uintptr_t)15;
+          const uintptr_t p1 = ((uintptr_t)base + b1) & ~(uintptr_t)15;
+          if (p1 > p0) prefetch_l2(reinterpret_cast<const void*>(p0), (unsigned)(p1 - p0));
+        };
+        if (lane < k) pf(U + (size_t)lane * a.np, c0 * 4, c1 * 4);
+        if (lane == 31 && fuse) {
+          if (a.xu8) pf(static_cast<const uint8_t*>(a.x) + sox, c0, c1);
+          else pf(Xg + sox, c0 * 4, c1 * 4);
+        }
+        if (lane == 30 && fuse && a.pipeline) pf(Mg + so, c0 * 4, c1 * 4);
+        if (lane == 29 && a.C == 1) pf(a.lab + (size_t)s * a.Pp, c0, c1);
+      }
       for (int slot = 0; slot < nslots; ++slot) {
         const int qi = slot * TG + lt;  // row group within the slice
         const bool ok = qi < qcount;
