@@ -30,6 +30,10 @@
 
 namespace prost {
 
+#ifndef PROST_TMA_ALT
+#define PROST_TMA_ALT 1  // alternate the tile order of consecutive U passes (ring_geometry)
+#endif
+
 constexpr int TT = 512;       // threads per CTA = coordinates per tile
 constexpr int TBOX = 256;     // tensor-map box width (box dims are <= 256)
 constexpr int NSTG = 3;       // tiles in flight per CTA
@@ -68,8 +72,9 @@ struct Ring {
   int side_es[NS];          // its element size (1 or 4)
   const uint8_t* lab;
   int k, row0, Pp, first, stride, ntiles;
+  bool rev;  // walk this CTA's tiles last to first (see ring_geometry)
 
-  __device__ __forceinline__ int tile_of(int i) const { return first + i * stride; }
+  __device__ __forceinline__ int tile_of(int i) const { return first + (rev ? ntiles - 1 - i : i) * stride; }
   __device__ __forceinline__ uint8_t* stage(int st) const { return base + (size_t)st * St::BYTES; }
   // basis value j of tile coordinate c (box c / TBOX lands as [k][TBOX])
   __device__ __forceinline__ float* urow(int st, int j, int c) const {
@@ -165,8 +170,18 @@ struct Ring {
   }
 };
 
+// Tile order: the chip walks the stream in bands of `chunks` tiles (band i =
+// every CTA's i-th tile).  Consecutive U passes alternate direction — pass 0
+// forward, CG iteration `it` backward when it is even, the plain geodesic
+// sweep backward, so with two iterations the passes run F, R, F, R and the
+// next frame's pass 0 F again — so each pass starts on the bands the previous
+// one finished with, which are still in L2 (126 MB against a 1 GB basis at
+// C4).  Passes with a reduction keep a fixed direction per pass (the partial
+// sums' order, and so the bits, do not depend on the previous pass).
 template <int K, int NS>
-__device__ __forceinline__ void ring_geometry(Ring<K, NS>& R, const Args& a, int s, const CUtensorMap* map) {
+__device__ __forceinline__ void ring_geometry(Ring<K, NS>& R, const Args& a, int s, const CUtensorMap* map,
+                                              bool rev = false) {
+  R.rev = rev;
   R.map = map;
   R.k = a.k;
   R.row0 = s * a.k;
@@ -285,13 +300,14 @@ __global__ void __launch_bounds__(TT, 1) k_iter_tma(const __grid_constant__ Args
   extern __shared__ __align__(128) uint8_t tsm[];
   const int s = a.s0 + blockIdx.y;
   Ctl* c = a.ctl + s;
-  __shared__ int go, lo;
+  __shared__ int go, lo, back;
   __shared__ double spend;
   __shared__ __align__(16) float sd[K];
   if (threadIdx.x == 0) {
     go = c->status == ST_OK && c->active;
     lo = c->gwin_lo;
     spend = c->pend_alpha;
+    back = PROST_TMA_ALT && (c->it % 2 == 0);
   }
   if (threadIdx.x < K) sd[threadIdx.x] = threadIdx.x < a.k ? (float)c->d[threadIdx.x] : 0.f;
   __syncthreads();
@@ -301,7 +317,7 @@ __global__ void __launch_bounds__(TT, 1) k_iter_tma(const __grid_constant__ Args
   __shared__ double sm[(TT / 32) * NV];
   __shared__ double red[NV];
   Ring<K, 2> R;
-  ring_geometry(R, a, s, &map);
+  ring_geometry(R, a, s, &map, back != 0);
   R.side[0] = static_cast<const uint8_t*>(a.r) + (size_t)s * a.np * 4;
   if (spend != 0.0) R.side[1] = static_cast<const uint8_t*>(a.ud) + (size_t)s * a.np * 4;
   R.start(tsm);
@@ -498,7 +514,9 @@ __global__ void __launch_bounds__(TT, 1) k_geo_tma(const __grid_constant__ Args 
   const bool need_r = FRES || do_geo;
   constexpr int NS = NEXT ? 5 : 4;
   Ring<K, NS> R;
-  ring_geometry(R, a, s, &map);
+  // backward, except when the next frame's pass 0 (a reduction) rides along:
+  // it keeps k_pass0_tma's forward order, bit for bit
+  ring_geometry(R, a, s, &map, PROST_TMA_ALT && !(NEXT && fu));
   if (need_r) R.side[0] = static_cast<const uint8_t*>(a.r) + (size_t)s * a.np * 4;
   if (need_r && moved) R.side[1] = static_cast<const uint8_t*>(a.ud) + (size_t)s * a.np * 4;
   if (do_lab) {
