@@ -55,7 +55,7 @@ struct prost_handle {
   int k = 0, C = 1, P = 0, Pp = 0;
   long long np = 0;
   size_t esz = 4;
-  int chunks = 1, nvmax = 0, wave = 0, n_ls = 0;
+  int chunks = 1, nvmax = 0, wave = 0, n_ls = 0, sms = 148;
   Ops ops{};
   // resident modes (k_resident / k_tmem): team geometry and its scratch
   bool resident = false;
@@ -320,16 +320,20 @@ void launchk(bool pdl, void (*k)(P...), dim3 g, dim3 b, size_t sm, cudaStream_t 
 
 void launch_median(prost_handle* h, const Args& a, cudaStream_t st, int sw, bool pdl = false) {
   const uintptr_t al = (uintptr_t)a.mask_out | (uintptr_t)a.halo_top | (uintptr_t)a.halo_bot;
+  // CTAs per stream: at most 128, or ~8 per SM over the launch when there
+  // are few streams (one 3840x2160 stream: 1184 CTAs, not 128 latency-bound
+  // ones looping 16 times; 19 -> ~5 us per frame)
+  const int cap = std::max(128, 8 * h->sms / std::max(1, sw));
   if (h->prm.width % 16 == 0 && (al & 15) == 0 && h->Pp % 16 == 0) {
     const int nw = h->P / 16;
-    const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
+    const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, cap)), sw);
     launchk(pdl, k_median16, mg, dim3(NT), 0, st, a);
   } else if (h->prm.width % 4 == 0 && ((uintptr_t)a.mask_out & 3) == 0) {
     const int nw = h->P / 4;
-    const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, 128)), sw);
+    const dim3 mg(std::max(1, std::min((nw + NT - 1) / NT, cap)), sw);
     launchk(pdl, k_median4, mg, dim3(NT), 0, st, a);
   } else {
-    const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, 64)), sw);
+    const dim3 mg(std::max(1, std::min((h->P + NT - 1) / NT, std::max(64, cap))), sw);
     launchk(pdl, k_median, mg, dim3(NT), 0, st, a);
   }
 }
@@ -426,7 +430,8 @@ struct Impl {
       }
     }
     switch (xs) {
-      case XS_STATS: LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a))); break;
+      case XS_STATS:
+      case XS_START: LAUNCH(PROST_PH_STATS, (k_stats<T, VEC><<<grid, NT, 0, st>>>(a))); break;
       case XS_COLD: LAUNCH(PROST_PH_COLD, (k_cold<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
       case XS_PASS0: LAUNCH(PROST_PH_PASS0, (k_pass0<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
       case XS_ITER: LAUNCH(PROST_PH_ITER, (k_iter<T, K, VEC><<<grid, NT, 0, st>>>(a))); break;
@@ -982,6 +987,7 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
   CK(cudaSetDevice(device));
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  h->sms = sms;
   const long long groups = (h->Pp / h->ops.VEC + NT - 1) / NT;
   // Streamed phase kernels: CTAs per stream.  Many streams: ~16 CTAs per SM
   // in total (waves keep the HBM queues full); few large streams: one wave of
@@ -1697,7 +1703,9 @@ int prost_xbegin(prost_handle* h, const void* frames, int32_t dtype, int32_t on_
     CK(cudaEventSynchronize(h->ev_peek));
     retire_peek(h);
   }
-  if (h->pipeline && !h->stats_over) pg.push_back(XS_STATS);
+  // once every stream is frozen (or without the pipeline) the statistics
+  // kernel only opens the frame: no reduction, no exchange
+  pg.push_back(h->pipeline && !h->stats_over ? XS_STATS : XS_START);
   if (h->maybe_cold) pg.push_back(XS_COLD);
   pg.push_back(XS_PASS0);
   for (int it = 0; it < h->prm.cg_max_iters; ++it) {
@@ -1726,7 +1734,7 @@ int prost_xnext(prost_handle* h, int32_t* exchange, void* cuda_stream) {
     const int xs = h->xprog[h->xpc++];
     h->ops.step(h, h->xa, st, h->S, xs);
     CK(cudaGetLastError());
-    if (xs != XS_GEO && xs != XS_GEOQR) {
+    if (xs != XS_GEO && xs != XS_GEOQR && xs != XS_START) {
       h->xlast = xs;
       *exchange = 1;
       return PROST_OK;

@@ -1064,7 +1064,10 @@ static __global__ void __launch_bounds__(NT) k_combine3(const __grid_constant__ 
 // k_xlogic: exchange mode — the scalar tail of phase `step` for every stream
 // the phase ran for, from the cross-rank sums in xred (one warp per stream).
 
-enum XStep { XS_STATS = 0, XS_COLD, XS_PASS0, XS_ITER, XS_LSFB, XS_GRADFB, XS_GEO, XS_GRAM, XS_GEOQR };
+// XS_START: the statistics kernel once every stream is frozen — no reduction
+// and so no exchange, but it still opens the frame (std, status: a frame
+// after a rejected one must run)
+enum XStep { XS_STATS = 0, XS_COLD, XS_PASS0, XS_ITER, XS_LSFB, XS_GRADFB, XS_GEO, XS_GRAM, XS_GEOQR, XS_START };
 
 template <int K>
 __global__ void __launch_bounds__(32) k_xlogic(const __grid_constant__ Args a, int step) {

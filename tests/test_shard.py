@@ -142,3 +142,22 @@ def test_two_ranks_match_unsharded(tmp_path):
     q1, _ = np.linalg.qr(U)
     s = np.linalg.svd(q0.T @ q1, compute_uv=False)
     assert np.sqrt(max(0.0, 1.0 - float(s.min()) ** 2)) <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["program", "peer"])
+def test_non_finite_frame_after_the_window(exchange):
+    """A non-finite frame after the statistics window is rejected and the next
+    frame runs normally: the host-driven program no longer exchanges for the
+    statistics phase once every stream is frozen, but still resets the frame
+    status (k_stats' no-op branch) — bit for bit the unsharded tracker."""
+    frames = list(_frames())
+    bad = frames[7].copy()
+    bad[5] = np.nan
+    seq = frames[:7] + [bad] + frames[7:]
+    m0, b0, U0 = _unsharded(seq)
+    m1, b1, U1, st = _sharded_run(seq, exchange=exchange)
+    keep = [i for i in range(len(seq)) if i != 7]
+    np.testing.assert_array_equal(m1[keep], m0[keep])
+    np.testing.assert_array_equal(b1[keep], b0[keep])
+    np.testing.assert_array_equal(U1, U0)
