@@ -328,6 +328,40 @@ def test_cluster_team_sums_match_global_slots(monkeypatch):
     np.testing.assert_array_equal(Ua, Ub)
 
 
+def test_slice_prefetch_does_not_change_results(monkeypatch):
+    """The L2 bulk prefetch of each slice's later slots (default on) only moves
+    data earlier: C3 shape, 12 streams (one round of 11 teams and a second),
+    bit-identical to PROST_PREFETCH=0."""
+    import torch
+
+    S, F = 12, 6
+    W, H = 320, 240
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=3, seed=0)
+    from paper_1302_2073_b200.synth import SceneStream, config_spec
+
+    frames = np.stack([SceneStream(config_spec("C3", s)).next_frames(F) for s in range(S)], 1)
+
+    def run():
+        bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
+        out = []
+        for f in range(F):
+            bt.push(torch.from_numpy(frames[f].astype(np.float32)).cuda(), background=bg, mask=mask)
+            out.append((mask.cpu().numpy().copy(), bg.cpu().numpy().copy()))
+        return out, bt.native.get_core_state(S - 1)[0]
+
+    monkeypatch.setenv("PROST_PREFETCH", "1")
+    a, Ua = run()
+    monkeypatch.setenv("PROST_PREFETCH", "0")
+    b, Ub = run()
+    for (ma, ba), (mb, bb) in zip(a, b):
+        np.testing.assert_array_equal(ma, mb)
+        np.testing.assert_array_equal(ba, bb)
+    np.testing.assert_array_equal(Ua, Ub)
+
+
 def test_large_batch_properties():
     """C3 shape (320x240, k=15) with 8 streams for 6 frames: size-independent
     properties — orthonormality, raw mask == threshold of the residual, mask ==
