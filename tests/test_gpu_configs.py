@@ -42,6 +42,7 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
+from oracle import prost_oracle as orc
 from parity import BatchRun, free_running, teacher_forced
 
 pytestmark = pytest.mark.gpu
@@ -276,3 +277,78 @@ def test_u8_frames_against_oracle():
                    r.fit.armijo_margin)
     print(w_free)
     assert w_free.bg_rel <= 1e-4 and w_free.sine <= 1e-3 and w_free.mask <= 1e-3
+
+
+# ---------------------------------------------------------------------------
+# BASELINE full sizes through size-independent properties (the oracle cannot
+# run 256 x 76,800 or 8.3M x 30 in test time): the threshold rule, the 3x3
+# majority, the background range, orthonormality of U, and — for the batch —
+# that a stream's result does not depend on the batch around it.
+
+def _full_run(name, S, F, i_init, seeds, frames):
+    import torch
+
+    from paper_1302_2073_b200.synth import CONFIGS
+
+    cfg = pkg.RunConfig(i_init=i_init, seed=0, **CONFIGS[name]["tracker"])
+    n = cfg.target_width * cfg.target_height
+    bt = pkg.BatchTracker(cfg, S, seeds=seeds)
+    mask = torch.empty((S, n), dtype=torch.uint8, device="cuda")
+    raw = torch.empty((S, n), dtype=torch.uint8, device="cuda")
+    res = torch.empty((S, n), dtype=torch.float32, device="cuda")
+    bg = torch.empty((S, n), dtype=torch.float32, device="cuda")
+    out = []
+    for f in range(F):
+        info = bt.push(frames[f], background=bg, residual=res, mask=mask, raw_mask=raw, fit=True)
+        assert all(info[s].frame_index == f + 1 and np.isfinite(info[s].fit_cost) for s in range(S))
+        # threshold rule (pipeline.py:196-213) on every pixel of every stream, on the device
+        # (compared in double, as the reference does: fp32(0.35) lies below 0.35)
+        assert torch.equal(raw, (res.double().abs() >= cfg.delta).to(torch.uint8))
+        assert float(bg.min()) >= 0.0 and float(bg.max()) <= 1.0
+        out.append((mask.clone(), raw.clone()))
+    return cfg, bt, out
+
+
+def _gram_error(U):
+    import torch
+
+    Ud = torch.from_numpy(np.ascontiguousarray(U)).cuda().double()
+    k = Ud.shape[1]
+    return float(torch.linalg.norm(Ud.T @ Ud - torch.eye(k, dtype=torch.float64, device="cuda")))
+
+
+def test_c3_full_batch_properties():
+    """All 256 C3 streams (320x240, k = 15, the benchmarked 11 x 13-CTA layout),
+    5 frames: properties on every stream; two streams re-run alone give the
+    same bits as inside the batch."""
+    import torch
+
+    from paper_1302_2073_b200.synth import DeviceScenes, config_spec
+
+    S, F, W, H = 256, 5, 320, 240
+    frames = DeviceScenes([config_spec("C3", s) for s in range(S)], "cuda:0", seed=7).next_frames(F)
+    cfg, bt, out = _full_run("C3", S, F, 3, list(range(S)), frames)
+    for s in (0, 37, 128, 255):  # the 3x3 majority (pipeline.py:215-228), sampled streams
+        for f in (0, F - 1):
+            np.testing.assert_array_equal(out[f][0][s].cpu().numpy(),
+                                          orc.majority3x3(out[f][1][s].cpu().numpy(), W, H))
+    for s in (0, 255):
+        assert _gram_error(bt.native.get_core_state(s)[0]) < 1e-4
+        _, alone, out1 = _full_run("C3", 1, F, 3, [s], frames[:, s:s + 1].contiguous())
+        for f in range(F):
+            assert torch.equal(out1[f][0][0], out[f][0][s]) and torch.equal(out1[f][1][0], out[f][1][s])
+        np.testing.assert_array_equal(alone.native.get_core_state(0)[0], bt.native.get_core_state(s)[0])
+
+
+def test_c4_full_frame_properties():
+    """One full C4 frame (3840x2160, k = 30, TMA-fed streamed kernels), 4 frames:
+    the threshold rule and the majority on all 8.3M pixels, U orthonormal."""
+    from paper_1302_2073_b200.synth import DeviceScenes, config_spec
+
+    F, W, H = 4, 3840, 2160
+    frames = DeviceScenes([config_spec("C4", 0)], "cuda:0", seed=7).next_frames(F)
+    cfg, bt, out = _full_run("C4", 1, F, 2, [0], frames)
+    for f in (0, F - 1):
+        np.testing.assert_array_equal(out[f][0][0].cpu().numpy(),
+                                      orc.majority3x3(out[f][1][0].cpu().numpy(), W, H))
+    assert _gram_error(bt.native.get_core_state(0)[0]) < 1e-4
