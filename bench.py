@@ -376,9 +376,17 @@ def main():
 
     preroll = cfg.i_init if args.preroll is None else args.preroll
     run_frames = c["frames"]  # frames per stream of the BASELINE run
-    e2e_frames = 0 if args.no_e2e else 2 + args.steps
-    nblock = 0 if args.block <= 1 else args.block * (max(1, args.steps // args.block) + 2)
+    # staged frames: every step a new frame, up to what fits comfortably in HBM
+    # (long runs cycle through the staged window after the pre-roll — a scene
+    # cut, which the tracker handles like any other frame); the e2e leg cycles
+    # through at most 64 pinned host frames
+    e2e_frames = 0 if args.no_e2e else min(2 + args.steps, 64)
+    nblock = 0 if args.block <= 1 else args.block * (max(1, min(args.steps // args.block, 12)) + 2)
     need = preroll + args.warmup + args.steps + 3 + e2e_frames + nblock
+    frame_bytes = len(stream_ids) * n * 4
+    need_full = need
+    need = min(need, max(preroll + args.warmup + 3 * max(args.block, 1) + 16,
+                         int(0.3 * torch.cuda.mem_get_info(dev)[0] / frame_bytes)))
     t_gen = time.perf_counter()
     if args.frames > 0:
         # a few distinct frames, cycled (numpy generator, bit-identical to the tests' streams)
@@ -409,6 +417,14 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     F = frames_dev.shape[0]
+    if host is None and F < need_full:
+        data_note += f" (a {need_full}-frame run: cycled through frames {preroll}..{F - 1} after that)"
+
+    def frame_at(i):
+        """Frame i of the run: the staged window, cycled after the pre-roll."""
+        if i < F:
+            return i
+        return i % F if F <= preroll + 1 else preroll + (i - preroll) % (F - preroll)
     from paper_1302_2073_b200 import _native as nat
 
     if pixel:
@@ -474,7 +490,7 @@ def main():
     for i in range(preroll):
         if i == 1:
             p0.record()
-        do_push(frames_dev[step % F], bg, mask)
+        do_push(frames_dev[frame_at(step)], bg, mask)
         step += 1
     p1.record()
     torch.cuda.synchronize()
@@ -484,7 +500,7 @@ def main():
     # launch of the process, stays out)
     ms_pre = max_over_ranks(p0.elapsed_time(p1)) if preroll > 1 else 0.0
     for _ in range(args.warmup):
-        do_push(frames_dev[step % F], bg, mask)
+        do_push(frames_dev[frame_at(step)], bg, mask)
         step += 1
     torch.cuda.synchronize()
     native.synchronize()
@@ -506,7 +522,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        do_push(frames_dev[step % F], bg, mask)
+        do_push(frames_dev[frame_at(step)], bg, mask)
         step += 1
     e1.record()
     torch.cuda.synchronize()
@@ -528,23 +544,33 @@ def main():
     if FB:
         bg_b = torch.empty((FB,) + tuple(bg.shape), dtype=bg.dtype, device=bg.device)
         mask_b = torch.empty((FB,) + tuple(mask.shape), dtype=mask.dtype, device=mask.device)
-        reps = max(1, args.steps // FB)
-        bt.push_many(frames_dev[step:step + FB], background=bg_b, mask=mask_b)
-        step += FB
+        reps = max(1, min(args.steps // FB, 12))
+
+        def block_at(i):  # F consecutive staged frames from i (or from the window start)
+            i = frame_at(i)
+            return i if i + FB <= F else preroll
+
+        s0 = block_at(step)
+        bt.push_many(frames_dev[s0:s0 + FB], background=bg_b, mask=mask_b)
+        step = s0 + FB
+        blocks = []
+        for _ in range(reps):
+            blocks.append(block_at(step))
+            step = blocks[-1] + FB
         torch.cuda.synchronize()
         barrier()
         e0.record()
-        for _ in range(reps):
-            bt.push_many(frames_dev[step:step + FB], background=bg_b, mask=mask_b)
-            step += FB
+        for b0 in blocks:
+            bt.push_many(frames_dev[b0:b0 + FB], background=bg_b, mask=mask_b)
         e1.record()
         torch.cuda.synchronize()
         barrier()
         ms_b = max_over_ranks(e0.elapsed_time(e1)) / (reps * FB)
         # per-phase split of one blocked call (separate, untimed)
         native.profile(True)
-        bt.push_many(frames_dev[step:step + FB], background=bg_b, mask=mask_b)
-        step += FB
+        s0 = block_at(step)
+        bt.push_many(frames_dev[s0:s0 + FB], background=bg_b, mask=mask_b)
+        step = s0 + FB
         torch.cuda.synchronize()
         ph_b = native.profile_read()
         native.profile(False)
@@ -564,7 +590,7 @@ def main():
     # per-phase breakdown (separate, untimed pass with events around launches)
     native.profile(True)
     for _ in range(3):
-        do_push(frames_dev[step % F], bg, mask)
+        do_push(frames_dev[frame_at(step)], bg, mask)
         step += 1
     torch.cuda.synchronize()
     phases = native.profile_read()
@@ -589,7 +615,7 @@ def main():
         else:
             # the e2e frames continue the streams: stage them in pinned host memory
             e2e0, HF = step, e2e_frames
-            src = frames_dev[e2e0:e2e0 + HF]
+            src = frames_dev[[frame_at(e2e0 + i) for i in range(HF)]]
         if u8:
             host_pinned = torch.empty(tuple(src.shape), dtype=torch.uint8, pin_memory=True)
             host_pinned.copy_(torch.clamp(torch.round(src.float() * 255.0), 0, 255).to(torch.uint8))
