@@ -56,7 +56,14 @@ def nxt():
     return host[i[0] % 30]
 
 
-print(f"device frames, device mask: {rate(lambda: bt.push(frames[100 + i[0] % 30], mask=mask_d)):.3f} ms")
+def nxt_dev(src):
+    i[0] += 1
+    return src[i[0] % 30]
+
+
+print(f"device frames, device mask: {rate(lambda: bt.push(nxt_dev(frames[100:130]), mask=mask_d)):.3f} ms")
+dev8 = host.cuda()
+print(f"device u8 frames, device mask: {rate(lambda: bt.push(nxt_dev(dev8), mask=mask_d)):.3f} ms")
 for label, kw in (("u8 in, nothing out", {}),
                   ("u8 in, mask", dict(mask=mask_h)),
                   ("u8 in, mask + raw", dict(mask=mask_h, raw_mask=raw_h)),
