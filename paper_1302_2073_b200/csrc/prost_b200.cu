@@ -822,7 +822,8 @@ int launch_frame(prost_handle* h, Args& a, cudaStream_t st) {
     // one cooperative launch for the whole frame of every stream, then the median
     const char* stg = getenv("PROST_STAGGER_NS");
     // k_tmem: L2 bulk prefetch of the rest of a CTA's slice at the start of its
-    // load (PROST_PREFETCH=0 turns it off; C3 1.182 -> 1.179 ms per step)
+    // load (PROST_PREFETCH=0 turns it off; within +-0.3% on C3: the load phase
+    // gains what the other teams' reductions lose)
     const char* pfe = getenv("PROST_PREFETCH");
     const char* alt = getenv("PROST_ALT");       // 0: slot groups load independently
     RArgs ra{h->rG, h->rT, h->rqpc, RES_RNV_MAX, h->rbar, h->rpart, h->S,
