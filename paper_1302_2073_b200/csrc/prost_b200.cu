@@ -1098,6 +1098,8 @@ int prost_create(const prost_params* params, int32_t n_streams, uint32_t flags, 
         h->rG = G;
         // enough teams for every stream to have a slot group, at most the chip
         h->rT = std::min((h->S + ng - 1) / ng, sms * TM_CPS / G);
+        if (const char* tenv = getenv("PROST_TM_T"))  // cap the teams (experiments)
+          if (atoi(tenv) > 0) h->rT = std::min(h->rT, atoi(tenv));
         h->resident_ops_K = K;
         if (h->C == 3) ALLOC(labc, S * np);
         ALLOC(rbar, (size_t)sms * TM_CPS * 2 * sizeof(unsigned));
