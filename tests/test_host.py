@@ -53,6 +53,9 @@ def test_create_validates_before_touching_the_device():
         (dict(channels=2), _native.ERR_DIMENSION),  # channels must be 1 or 3
         (dict(max_backtracks=100), _native.ERR_CONFIG),
         (dict(width=2, height=1, channels=1), _native.ERR_DIMENSION),  # k >= n
+        (dict(width=0), _native.ERR_DIMENSION),     # empty frame
+        (dict(cg_max_iters=0), _native.ERR_CONFIG),
+        (dict(shrink=1.0), _native.ERR_CONFIG),
     ]
     for override, code in cases:
         p = to_native(good, 8, 6, 1, 10)
@@ -63,6 +66,11 @@ def test_create_validates_before_touching_the_device():
         assert rc == code, (override, rc)
         assert _native.last_error(h)
         lib.prost_destroy(h)
+    # an empty batch
+    h = ctypes.c_void_p()
+    assert lib.prost_create(ctypes.byref(to_native(good, 8, 6, 1, 10)), 0, 0, 0, ctypes.byref(h)) == \
+        _native.ERR_CONFIG
+    lib.prost_destroy(h)
 
 
 def test_param_mirrors_match_reference_semantics():
