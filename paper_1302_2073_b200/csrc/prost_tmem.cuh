@@ -972,12 +972,16 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
                 const float h = rsqrtf(b);
                 const float q = rsqrtf(h);
                 cst[m] = fmaf(q, w[e], cst[m]);
-                gm[m] = 0.5f * t * (q * w[e]) * (h * h);
+                // twice the coordinate gradient (cost.py:103-112 without its
+                // factor 1/2): exactly 2x in fp32, and so are the gradient sums
+                // built from it; the scalar logic halves them (exact) — one
+                // multiply fewer per trial
+                gm[m] = t * (q * w[e]) * (h * h);
               } else {
                 float tw, gg;
                 penalty_t<PM>(t, w[e], a, tw, gg);
                 cst[m] += tw;
-                gm[m] = gg;
+                gm[m] = 2.f * gg;
               }
             }
             float gs[WG];
@@ -1010,6 +1014,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
         {
           const unsigned long long tli = (ra.prof && tid == 0) ? ptimer() : 0;
+          if (lt < 32) {  // the sweep summed 2 g (and 4 g^2): exact halving in double
+            for (int v = WC + lt; v < NV; v += 32) red[v] *= ((v - WC) % (K + 1) == K) ? 0.25 : 0.5;
+            __syncwarp();
+          }
           LOGIC(TM_AFTER_ITER<K>(cs, a, s, lt, red, wlo));
           if (ra.prof && tid == 0) sprof[PROF_LOGIC_ITER] += ptimer() - tli;
         }
