@@ -723,9 +723,15 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         const bool ok = qi < qcount;
         const int coord = (q0 + qi) * 4, pix = pixel_of(coord);
         float4 p[K];
+        if (ok && k == K) {  // the common case: every plane, no per-plane predicate or zero fill
+          const float* Uc = U + coord;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-          p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + coord)) : z4;
+          for (int j = 0; j < K; ++j) p[j] = __ldcs(reinterpret_cast<const float4*>(Uc + (size_t)j * a.np));
+        } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            p[j] = (ok && j < k) ? __ldcs(reinterpret_cast<const float4*>(U + (size_t)j * a.np + coord)) : z4;
+        }
         const uint32_t lb = ok ? *reinterpret_cast<const uint32_t*>(a.lab + (size_t)s * a.Pp + pix) : 0u;
         if (!WCOL) sL[qi] = lb;
         float xh[4], w[4], r[4], uy[4];
