@@ -59,6 +59,17 @@ enum StreamStatus { ST_OK = 0, ST_NONFINITE = 3 };
 
 // Per-stream control block: everything the scalar part of the algorithm
 // carries between phases (double precision throughout).
+// An 8-bit intensity as the reference reads it, float(b / 255) (frameio.py:136:
+// the double product b * (1/255) rounded to fp32), in four fp32 instructions:
+// q = b * fl(1/255) corrected once by its exact FMA residual.  Equal to the
+// double expression for all 256 values (checked exhaustively: tests/test_host.py).
+__device__ __forceinline__ float u8_unit(unsigned b) {
+  constexpr float R = 1.0f / 255.0f;
+  const float bf = (float)b;
+  const float q = __fmul_rn(bf, R);
+  return fmaf(fmaf(-q, 255.0f, bf), R, q);
+}
+
 struct Ctl {
   double y[KMAX], d[KMAX], grad[KMAX], v[KMAX];
   double f;            // current cost (fit.py f_cur)

@@ -207,7 +207,7 @@ __device__ __forceinline__ float tile_weight(const Args& a, int pix, uint8_t l) 
 __device__ __forceinline__ float tile_xhat(const Args& a, const uint8_t* xs, const float* ms, int c,
                                            float* M, int pix, bool upd, float seen, float stdv,
                                            bool& bad) {
-  const float xv = a.xu8 ? (float)((double)xs[c] * (1.0 / 255.0)) : reinterpret_cast<const float*>(xs)[c];
+  const float xv = a.xu8 ? u8_unit(xs[c]) : reinterpret_cast<const float*>(xs)[c];
   bad |= !isfinite(xv);
   if (!a.pipeline) return xv;
   float mv = ms[c];

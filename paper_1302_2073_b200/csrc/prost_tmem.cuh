@@ -420,14 +420,14 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   const float* Mg = static_cast<const float*>(a.mean);
   const float* Xg = static_cast<const float*>(a.x);
   // 4 frame values at coordinate offset off: fp32, or 8-bit divided by 255
-  // exactly as the conversion kernel k_pack does (double product, rounded)
+  // exactly as the conversion kernel k_pack does (u8_unit: the double product, rounded)
   auto ld_x4 = [&](size_t off, float (&xv)[4]) {
     if (a.xu8) {
       const uchar4 b = *reinterpret_cast<const uchar4*>(static_cast<const uint8_t*>(a.x) + off);
-      xv[0] = (float)((double)b.x * (1.0 / 255.0));
-      xv[1] = (float)((double)b.y * (1.0 / 255.0));
-      xv[2] = (float)((double)b.z * (1.0 / 255.0));
-      xv[3] = (float)((double)b.w * (1.0 / 255.0));
+      xv[0] = u8_unit(b.x);
+      xv[1] = u8_unit(b.y);
+      xv[2] = u8_unit(b.z);
+      xv[3] = u8_unit(b.w);
     } else {
       f4(*reinterpret_cast<const float4*>(Xg + off), xv);
     }

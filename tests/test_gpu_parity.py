@@ -536,6 +536,7 @@ def test_u8_frame_ingest(k):
                         target_height=H, grayscale=True, i_init=3, seed=0)
     data = np.stack([c0_stream(F, W, H, seed=s) for s in range(S)], 1)
     q = np.clip(np.rint(data * 255.0), 0, 255).astype(np.uint8)
+    q[0, 0, :256] = np.arange(256)  # every 8-bit value through the device conversion
     scaled = (q.astype(np.float64) * (1.0 / 255.0)).astype(np.float32)
     outs = []
     for frames in (q, scaled):

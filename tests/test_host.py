@@ -138,3 +138,27 @@ def test_bench_byte_model():
     assert bench.b_alg(19200, 15, 19200) == 2_592_000
     assert bench.b_alg(230400, 15, 76800) == 30_643_200
     assert bench.b_alg(76800, 15, 76800) == 10_368_000
+
+
+def test_u8_unit_formula_is_exact():
+    """The kernels' 8-bit conversion (u8_unit, prost_kernels.cuh): q = b * fl(1/255),
+    then one FMA-residual correction — equal to the reference's float(b / 255)
+    (frameio.py:136: the double product rounded to fp32) for all 256 values.
+    FMAs evaluated exactly in rationals, rounded once to fp32."""
+    from fractions import Fraction
+
+    def round32(v: Fraction) -> np.float32:
+        x = np.float32(float(v))
+        cands = [np.nextafter(x, np.float32(-np.inf)), x, np.nextafter(x, np.float32(np.inf))]
+        return min(cands, key=lambda c: (abs(Fraction(float(c)) - v),
+                                         int(np.array(c, dtype=np.float32).view(np.uint32)) & 1))
+
+    def fma(a, b, c):
+        return round32(Fraction(float(a)) * Fraction(float(b)) + Fraction(float(c)))
+
+    r = np.float32(1.0 / 255.0)
+    for b in range(256):
+        bf = np.float32(b)
+        q = np.float32(bf * r)
+        got = fma(fma(-q, np.float32(255.0), bf), r, q)
+        assert got == np.float32(b * (1.0 / 255.0)), b
