@@ -333,7 +333,7 @@ struct SmemRows {
   __device__ __forceinline__ void operator()(int e, float (&u)[RS]) const {
 #pragma unroll
     for (int g4 = 0; g4 < RS / 4; ++g4) {
-      const float4 t = ok ? base[(size_t)(e * (RS / 4) + g4) * qs] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 t = base[(size_t)(e * (RS / 4) + g4) * qs];  // (the sweep skips rows past the slice)
       u[4 * g4] = t.x; u[4 * g4 + 1] = t.y; u[4 * g4 + 2] = t.z; u[4 * g4 + 3] = t.w;
     }
   }
@@ -481,8 +481,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     for (int slot = 0; slot < nst; ++slot)
       body(slot * TG + lt, TmemRows<RS>{tbase + (unsigned)(slot * QW)});
     for (int slot = QT; slot < nslots; ++slot) {
-      const int qi = slot * TG + lt;  // rows past qcount were never loaded
-      body(qi, SmemRows<RS>{sU + (qi - QT * TG), qs, qi < qcount});
+      // rows past qcount were never loaded and hold nothing: skipped (their
+      // contributions are exact zeros — weight 0 — and nothing reads their r)
+      const int qi = slot * TG + lt;
+      if (qi < qcount) body(qi, SmemRows<RS>{sU + (qi - QT * TG), qs, true});
     }
   };
   const float omega = a.omegaf;
