@@ -71,6 +71,11 @@ class ShardedTracker:
     the unsharded tracker.
     """
 
+    # Test hook: issue the collectives even at world size 1 (an NCCL group of
+    # one rank on one GPU runs the same all-reduce / all-gather calls, stream
+    # ordering included, as a multi-GPU group — the only NCCL shape one GPU has)
+    collectives_at_world1 = False
+
     def __init__(self, config: RunConfig, group=None, i_init: Optional[int] = None, *,
                  precision: str = "fp32", device: int = 0, seed: Optional[int] = None,
                  basis: Optional[np.ndarray] = None, exchange: str = "program"):
@@ -145,7 +150,7 @@ class ShardedTracker:
         return torch.cuda.stream(torch.cuda.ExternalStream(cuda_stream, device=self.device))
 
     def _allreduce(self, t):
-        if self.world == 1:
+        if self.world == 1 and not self.collectives_at_world1:
             return
         if self.backend == "nccl":
             self.dist.all_reduce(t, group=self.group)
@@ -155,7 +160,7 @@ class ShardedTracker:
             t.copy_(h)
 
     def _allgather_edges(self):
-        if self.world == 1:
+        if self.world == 1 and not self.collectives_at_world1:
             return
         if self.backend == "nccl":
             self.dist.all_gather_into_tensor(self.gathered, self.edges, group=self.group)
@@ -182,7 +187,7 @@ class ShardedTracker:
             self.exchanges += 1
             nt.xapply(cuda_stream)
         halo_top = halo_bot = None
-        if mask is not None and self.world > 1:
+        if mask is not None and (self.world > 1 or self.collectives_at_world1):
             nt.xedges(self.edges[0].data_ptr(), self.edges[1].data_ptr(), cuda_stream)
             with self._on(cuda_stream):
                 self._allgather_edges()

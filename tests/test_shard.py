@@ -161,3 +161,55 @@ def test_non_finite_frame_after_the_window(exchange):
     np.testing.assert_array_equal(m1[keep], m0[keep])
     np.testing.assert_array_equal(b1[keep], b0[keep])
     np.testing.assert_array_equal(U1, U0)
+
+
+def _nccl_worker(rank, port, frames, out):
+    """One-rank NCCL group: the exchange program's all-reduces and the halo
+    all-gather go through NCCL on a side CUDA stream (shard.py _on)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1302_2073_b200.shard import ShardedTracker
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    ShardedTracker.collectives_at_world1 = True
+    st = ShardedTracker(_cfg())
+    assert st.backend == "nccl"
+    side = torch.cuda.Stream()
+    n = st.rows * W
+    mask = torch.empty(n, dtype=torch.uint8, device="cuda")
+    bg = torch.empty(n, dtype=torch.float32, device="cuda")
+    masks, bgs = [], []
+    for f in frames:
+        blk = torch.from_numpy(st.local_rows(f)).cuda()
+        torch.cuda.synchronize()
+        st.push(blk, background=bg, mask=mask, cuda_stream=side.cuda_stream)
+        side.synchronize()
+        masks.append(mask.cpu().numpy().copy())
+        bgs.append(bg.cpu().numpy().copy())
+    torch.cuda.synchronize()
+    np.savez(out, m=np.array(masks), b=np.array(bgs), U=st.get_basis_block(), ex=st.exchanges)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_exchange_program_world1_matches_unsharded_bitwise(tmp_path):
+    """The NCCL branch of the exchange program (all_reduce of the exchange
+    buffer, all_gather of the label edges) on a non-default CUDA stream: a
+    one-rank sum is the identity, so the run is bit-identical to the unsharded
+    tracker, and every phase that can run was exchanged through NCCL."""
+    import torch.multiprocessing as mp
+
+    frames = _frames()
+    m0, b0, U0 = _unsharded(frames)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "nccl.npz")
+    mp.spawn(_nccl_worker, args=(port, frames, out), nprocs=1, join=True)
+    r = np.load(out)
+    assert int(r["ex"]) >= 3 * F
+    np.testing.assert_array_equal(r["m"], m0)
+    np.testing.assert_array_equal(r["b"], b0)
+    np.testing.assert_array_equal(r["U"], U0)
