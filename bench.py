@@ -41,7 +41,7 @@ PHASE_BYTES_NOTE = "per-phase algorithmic bytes per stream-frame launch"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
@@ -126,8 +126,24 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the sampler's first line can take a while on a fresh box: start
+            # the timed region only once it is producing samples
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10.0 and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+
+    def mark(self):
+        """Samples so far (call at the start of the timed region)."""
+        return len(self.lines)
+
+    def wait_one_more(self, n0, limit=1.0):
+        """Wait (bounded) for a sample taken after the timed region started, so
+        a short region still has one sample at or after its end."""
+        t0 = time.time()
+        while len(self.lines) <= n0 and time.time() - t0 < limit and self.proc is not None:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -508,7 +524,6 @@ def main():
     clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)).split(",")[0])
                     if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit() else dev)
     clocks.start()
-    time.sleep(0.3)
     launches0 = native.launches
     def exchanges_so_far():
         if not pixel:
@@ -520,6 +535,7 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    n_clk0 = clocks.mark()
     e0.record()
     for _ in range(args.steps):
         do_push(frames_dev[frame_at(step)], bg, mask)
@@ -530,6 +546,7 @@ def main():
     ms = e0.elapsed_time(e1)
     launches = native.launches - launches0
     ex_timed = (exchanges_so_far() - ex0) / args.steps if pixel else None
+    clocks.wait_one_more(n_clk0)
     clk = clocks.stop()
     ms = max_over_ranks(ms)
     ms_step = ms / args.steps

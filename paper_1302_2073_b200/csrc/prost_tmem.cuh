@@ -27,6 +27,10 @@
 #include <type_traits>
 
 #include "prost_logic_fast.cuh"
+// Timing counters (RArgs.prof, the bench's counters pass) only in the PROF
+// instances: the timer values live across the sweeps, and in the 128-register
+// kernel they cost spills (stack 152 -> 128 B, C3 1.143 -> 1.109 ms per step)
+#define TM_PROF_ON(r) (PROF && (r).prof != nullptr)
 #ifndef PROST_FAST_LOGIC
 #define PROST_FAST_LOGIC 1
 #endif
@@ -127,7 +131,7 @@ __device__ __forceinline__ void group_sync(int g) {
 // the same order as the global-slot path (lane = rank, then the warp
 // butterfly), so both give the same bits.
 constexpr int CL_NV = 64;
-template <int NG, bool CL = false>
+template <int NG, bool CL = false, bool PROF = false>
 __device__ __forceinline__ void team_sum_g(const RArgs& ra, int vt, int VT, int rank, int g, int lt,
                                            const double* wred, int nv, double* red, unsigned& epoch,
                                            unsigned long long* sprof) {
@@ -136,7 +140,7 @@ __device__ __forceinline__ void team_sum_g(const RArgs& ra, int vt, int VT, int 
     static_assert(NG == 1, "cluster team sums: one slot group");
     __shared__ double cpart[2][CL_NV];
     __syncthreads();
-    const bool tp = ra.prof && lt == 0;
+    const bool tp = TM_PROF_ON(ra) && lt == 0;
     const unsigned long long t0 = tp ? ptimer() : 0;
     const int warp = lt >> 5, lane = lt & 31;
     const int par = epoch & 1;
@@ -182,7 +186,7 @@ __device__ __forceinline__ void team_sum_g(const RArgs& ra, int vt, int VT, int 
     return;
   }
   group_sync<NG>(g);
-  const bool tp = ra.prof && g == 0 && lt == 0;
+  const bool tp = TM_PROF_ON(ra) && g == 0 && lt == 0;
   unsigned long long t0 = tp ? ptimer() : 0;
   const int warp = lt >> 5, lane = lt & 31;
   const int G = ra.G;
@@ -371,7 +375,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
 // the groups' slice loads alternate A, B, A, B, ...).
 // BLK: the frame-blocking instance (prost_push_many); the single-frame
 // instance compiles the blocking paths out (they cost registers).
-template <int K, int PM, int NG, bool BLK, bool CL = false>
+template <int K, int PM, int NG, bool BLK, bool CL = false, bool PROF = false>
 __global__ void __launch_bounds__(TM_NT, TM_CPS)
     k_tmem(const __grid_constant__ Args a, const __grid_constant__ RArgs ra) {
   using Geo = TmemGeom<K>;
@@ -466,13 +470,13 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
   } while (0)
 #define LOGIC(call)                                                        \
   do {                                                                     \
-    const unsigned long long tl0 = (ra.prof && tid == 0) ? ptimer() : 0;   \
+    const unsigned long long tl0 = (TM_PROF_ON(ra) && tid == 0) ? ptimer() : 0;   \
     if (lt < 32) {                                                         \
       call;                                                                \
       __syncwarp();                                                        \
       SYNC_FLOATS();                                                       \
     }                                                                      \
-    if (ra.prof && tid == 0) sprof[PROF_LOGIC] += ptimer() - tl0;          \
+    if (TM_PROF_ON(ra) && tid == 0) sprof[PROF_LOGIC] += ptimer() - tl0;          \
   } while (0)
 
   // Visit every row group of this thread: body(qi, rows).  TMEM row groups
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #else
   for (int s = vt; s < ra.S; s += VT, ++round) {
 #endif
-    if (ra.prof && tid == 0) sprof[PROF_ROUNDS] += 1;
+    if (TM_PROF_ON(ra) && tid == 0) sprof[PROF_ROUNDS] += 1;
     if (NG > 1 && ra.alt) {
       // the groups' slice loads alternate: A0 B0 A1 B1 ... (a finished group
       // no longer holds the other back)
@@ -579,10 +583,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       cs->info_slot = 0;
     }
 
-    unsigned long long tph = (ra.prof && tid == 0) ? ptimer() : 0;
+    unsigned long long tph = (TM_PROF_ON(ra) && tid == 0) ? ptimer() : 0;
 #define PHASE_MARK(idx)                              \
   do {                                               \
-    if (ra.prof && tid == 0) {                       \
+    if (TM_PROF_ON(ra) && tid == 0) {                       \
       const unsigned long long tn = ptimer();        \
       sprof[idx] += tn - tph;                        \
       tph = tn;                                      \
@@ -612,7 +616,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       rstage_g(s1, wred, 0, 3, lt);
       rstage_g(s2, wred, 1, 3, lt);
       rstage_g(nf, wred, 2, 3, lt);
-      team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, 3, red, epoch, sprof);
+      team_sum_g<NG, CL, PROF>(ra, vt, VT, rank, g, lt, wred, 3, red, epoch, sprof);
       if (lt == 0) {
         if (red[2] > 0.0) {
           cs->status = ST_NONFINITE;
@@ -698,7 +702,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
     for (int j = 0; j <= K; ++j) pk[j] = use_p0 ? pk_n[j] : 0.f;
     p0_ready = false;
     if (frame_ok && f == 0) {
-      const unsigned long long tw0 = (ra.prof && tid == 0) ? ptimer() : 0;
+      const unsigned long long tw0 = (TM_PROF_ON(ra) && tid == 0) ? ptimer() : 0;
       const float* U = static_cast<const float*>(a.U) + (size_t)s * k * a.np;
       // The slots after the first arrive through L2: one bulk prefetch per
       // basis plane (and for the frame / mean / label bytes) of the rest of
@@ -780,10 +784,10 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
       tmem_wait_st();
       if (fuse) mean_pending = false;
       group_sync<NG>(g);  // shared-memory rows, r and u_dir visible to every warp
-      if (ra.prof && tid == 0) sprof[PROF_PREFETCH] += ptimer() - tw0;
+      if (TM_PROF_ON(ra) && tid == 0) sprof[PROF_PREFETCH] += ptimer() - tw0;
     }
     if (NG > 1 && lt == 0) s_loads[g] = round + 1;
-    tph = (ra.prof && tid == 0) ? ptimer() : 0;
+    tph = (TM_PROF_ON(ra) && tid == 0) ? ptimer() : 0;
 
     if (frame_ok) {
       // ---- cold start y = U^T x (fit.py:86-87), then pass 0 over the slice ---
@@ -808,7 +812,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         mean_pending = false;
         stage_floats_g<K>(pkc, wred, K + 1, 0, lt);
         rstage_g(bad ? 1.0 : 0.0, wred, K, K + 1, lt);
-        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
+        team_sum_g<NG, CL, PROF>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
         if (lt < 32) {
           if (red[K] > 0.0) mark_nonfinite(cs, a, s, lt);
           else if (lt < k) cs->y[lt] = red[lt];
@@ -848,7 +852,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         rstage_g(cost, wred, 0, K + 3, lt);
         stage_floats_g<K + 1>(pk, wred, K + 3, 1, lt);
         rstage_g(bad ? 1.0 : 0.0, wred, K + 2, K + 3, lt);
-        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, K + 3, red, epoch, sprof);
+        team_sum_g<NG, CL, PROF>(ra, vt, VT, rank, g, lt, wred, K + 3, red, epoch, sprof);
         LOGIC(TM_AFTER_PASS0<K>(cs, a, s, lt, red));
         group_sync<NG>(g);
       }
@@ -896,7 +900,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         });
 #pragma unroll
         for (int m = 0; m < LSW; ++m) rstage_g((double)cst[m], wred, m, LSW, lt);
-        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, LSW, red, epoch, sprof);
+        team_sum_g<NG, CL, PROF>(ra, vt, VT, rank, g, lt, wred, LSW, red, epoch, sprof);
         LOGIC(TM_AFTER_LSFB(cs, a, s, lt, red, base));
       } else if (cs->need_gradfb) {
         const float al = (float)cs->acc_alpha;
@@ -921,7 +925,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
           }
         });
         stage_floats_g<K + 1>(pk, wred, K + 1, 0, lt);
-        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
+        team_sum_g<NG, CL, PROF>(ra, vt, VT, rank, g, lt, wred, K + 1, red, epoch, sprof);
         LOGIC(TM_AFTER_GRADFB<K>(cs, a, s, lt, red));
       } else {
         constexpr int NV = WC + WG * (K + 1);
@@ -950,7 +954,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
         // instead of 8 MUFU and ~30 selects per row).
         static_assert(WC <= 4 && WG <= 2 && WC - WG <= 2, "window positions");
         const bool w1 = wlo >= 1, w2 = wlo >= 2;
-        const unsigned long long tsw0 = (ra.prof && tid == 0) ? ptimer() : 0;
+        const unsigned long long tsw0 = (TM_PROF_ON(ra) && tid == 0) ? ptimer() : 0;
         sweep([&](int qi, const auto& rows) {
           float r[4], w[4], udo[4], ud[4];
           f4(sR[qi], r);
@@ -1009,7 +1013,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #pragma unroll
         for (int m = 0; m < WC; ++m) rstage_g((double)cst[m], wred, m, NV, lt);
         stage_floats_g<WG * (K + 1)>(pk, wred, NV, WC, lt);
-        if (ra.prof) {  // (uniform: every thread of the group takes the barrier)
+        if (TM_PROF_ON(ra)) {  // (uniform: every thread of the group takes the barrier)
           const unsigned long long t1 = tid == 0 ? ptimer() : 0;
           group_sync<NG>(g);
           if (tid == 0) {
@@ -1019,15 +1023,15 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #endif
           }
         }
-        team_sum_g<NG, CL>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
+        team_sum_g<NG, CL, PROF>(ra, vt, VT, rank, g, lt, wred, NV, red, epoch, sprof);
         {
-          const unsigned long long tli = (ra.prof && tid == 0) ? ptimer() : 0;
+          const unsigned long long tli = (TM_PROF_ON(ra) && tid == 0) ? ptimer() : 0;
           if (lt < 32) {  // the sweep summed 2 g (and 4 g^2): exact halving in double
             for (int v = WC + lt; v < NV; v += 32) red[v] *= ((v - WC) % (K + 1) == K) ? 0.25 : 0.5;
             __syncwarp();
           }
           LOGIC(TM_AFTER_ITER<K>(cs, a, s, lt, red, wlo));
-          if (ra.prof && tid == 0) sprof[PROF_LOGIC_ITER] += ptimer() - tli;
+          if (TM_PROF_ON(ra) && tid == 0) sprof[PROF_LOGIC_ITER] += ptimer() - tli;
         }
       }
       group_sync<NG>(g);
@@ -1233,7 +1237,7 @@ __global__ void __launch_bounds__(TM_NT, TM_CPS)
 #undef SYNC_FLOATS
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (ra.prof && tid == 0) {
+  if (TM_PROF_ON(ra) && tid == 0) {
     sprof[PROF_TOTAL] = ptimer() - t_start;
     sprof[PROF_GT_TOTAL] = gtimer() - g_start;
     for (int i = 0; i < PROF_N; ++i) ra.prof[(size_t)blockIdx.x * PROF_N + i] = sprof[i];

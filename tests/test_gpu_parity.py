@@ -362,6 +362,42 @@ def test_slice_prefetch_does_not_change_results(monkeypatch):
     np.testing.assert_array_equal(Ua, Ub)
 
 
+def test_profiled_instance_matches(monkeypatch):
+    """The k_tmem instance with the timing counters (profile(True), the
+    bench's counters pass) computes the same bits as the counter-free one the
+    frames normally run on: C3 shape, 12 streams, frames alternating between
+    the two instances."""
+    import torch
+    from paper_1302_2073_b200.synth import SceneStream, config_spec
+
+    S, F = 12, 6
+    W, H = 320, 240
+    cfg = pkg.RunConfig(subspace_dim=15, p=0.5, mu=1e-4, cg_max_iters=2, target_width=W,
+                        target_height=H, grayscale=True, i_init=3, seed=0)
+    frames = np.stack([SceneStream(config_spec("C3", s)).next_frames(F) for s in range(S)], 1)
+
+    def run(alternate):
+        bt = pkg.BatchTracker(cfg, S, seeds=list(range(S)))
+        mask = torch.empty((S, W * H), dtype=torch.uint8, device="cuda")
+        bg = torch.empty((S, W * H), dtype=torch.float32, device="cuda")
+        out = []
+        for f in range(F):
+            bt.native.profile(alternate and f % 2 == 1)
+            bt.push(torch.from_numpy(frames[f].astype(np.float32)).cuda(), background=bg, mask=mask)
+            out.append((mask.cpu().numpy().copy(), bg.cpu().numpy().copy()))
+        if alternate:  # the last profiled launch wrote its per-CTA counters
+            assert bt.native.resident_counters()["rounds"] > 0
+        bt.native.profile(False)
+        return out, bt.native.get_core_state(S - 1)[0]
+
+    a, Ua = run(False)
+    b, Ub = run(True)
+    for (ma, ba), (mb, bb) in zip(a, b):
+        np.testing.assert_array_equal(ma, mb)
+        np.testing.assert_array_equal(ba, bb)
+    np.testing.assert_array_equal(Ua, Ub)
+
+
 def test_large_batch_properties():
     """C3 shape (320x240, k=15) with 8 streams for 6 frames: size-independent
     properties — orthonormality, raw mask == threshold of the residual, mask ==
