@@ -198,7 +198,9 @@ int prost_query(prost_handle* h, int32_t what, int64_t* value);
 #define PROST_PH_FRAME 9   /* the register-resident whole-frame kernel */
 #define PROST_N_PHASES 10
 int prost_profile(prost_handle* h, int32_t enable);
-/* Resident-kernel timing of the last launch made with profiling on, as
+/* With profiling on, the TMEM-resident frame kernel runs its counter instance
+ * (same results bit for bit; the counter-free instance that runs otherwise is
+ * ~3% faster).  Resident-kernel timing of the last launch made with profiling on, as
  * per-CTA means (%globaltimer ns): [0] kernel, [1] team-barrier waits,
  * [2] slot reads, [3] scalar logic, [4] prefetch waits, [5] team reductions,
  * [6] rounds, [7] unused, [8] (if n > 8) the slowest CTA's kernel time. */
