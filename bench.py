@@ -396,7 +396,7 @@ def main():
     # (long runs cycle through the staged window after the pre-roll — a scene
     # cut, which the tracker handles like any other frame); the e2e leg cycles
     # through at most 64 pinned host frames
-    e2e_frames = 0 if args.no_e2e else min(2 + args.steps, 64)
+    e2e_frames = 0 if args.no_e2e else min(max(2, args.warmup) + args.steps, 64)
     nblock = 0 if args.block <= 1 else args.block * (max(1, min(args.steps // args.block, 12)) + 2)
     need = preroll + args.warmup + args.steps + 3 + e2e_frames + nblock
     frame_bytes = len(stream_ids) * n * 4
@@ -651,7 +651,7 @@ def main():
             else:
                 bt.push(frame, background=bg_h, mask=mask_h, raw_mask=raw_h, fit_out=fit_h)
 
-        for _ in range(2):
+        for _ in range(max(2, args.warmup)):  # untimed: the host-I/O path's own warm-up
             push_e2e(host_pinned[(step - e2e0) % HF])
             step += 1
         torch.cuda.synchronize()
